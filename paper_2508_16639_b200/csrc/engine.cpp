@@ -1,0 +1,875 @@
+// engine.cpp — host side of the B200 ESCG engine and its C ABI (include/escg_dev.h).
+//
+// Mirrors the reference's dispatcher/driver layer (engine.cpp:194-240 simulate, :96-192 run loops,
+// :47-57 record_and_check) around the sm_100a kernels in kernels.cu.  Validation mirrors
+// params.hpp:37-48 and dominance.cpp:8-21 with the same messages; errors become int codes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/escg_dev.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void config_error(const std::string& m) { throw Error(ESCG_ECONFIG, m); }
+[[noreturn]] void engine_error(const std::string& m) { throw Error(ESCG_EENGINE, m); }
+
+#define CK(expr)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (expr);                                                                  \
+        if (e_ != cudaSuccess) engine_error(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return ESCG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return ESCG_EENGINE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return ESCG_EENGINE;
+    }
+}
+
+// ---- validation (params.hpp:37-48, dominance.cpp:8-21) ---------------------------------------
+
+void validate_params(const escg_params& p) {
+    if (p.length < 2 || p.height < 2) config_error("lattice dimensions must be at least 2x2");
+    if (p.mcs_limit < 0) config_error("mcs limit must be non-negative");
+    if (p.print_frequency < 1) config_error("print frequency must be positive");
+    if (!(p.mobility >= 0.0)) config_error("mobility must be non-negative");
+    if (p.species < 1 || p.species > 64) config_error("species count must be in [1, 64]");
+    if (static_cast<int64_t>(p.length) * p.height > (int64_t{1} << 31))
+        config_error("lattice exceeds the supported cell count");
+    if (!(p.empty_prob >= 0.0 && p.empty_prob <= 1.0)) config_error("empty probability must be in [0, 1]");
+    if (p.num_randoms < 1) config_error("numRandoms must be positive");
+    if (p.neighbourhood != 4 && p.neighbourhood != 8) config_error("neighbourhood must be 4 or 8");
+}
+
+void validate_dominance(const double* dom, int S, int kind) {
+    if (S < 1 || S > 64) config_error("dominance size must be in [1, 64]");
+    if (!dom) config_error("dominance entry count does not match size");
+    for (int i = 0; i < S; ++i)
+        if (dom[static_cast<size_t>(i) * S + i] != 0.0)
+            config_error("dominance diagonal must be zero (species " + std::to_string(i + 1) + ")");
+    for (int i = 0; i < S * S; ++i) {
+        const double v = dom[i];
+        if (!(v >= 0.0 && v <= 1.0)) config_error("dominance entries must lie in [0, 1]");
+        if (kind == ESCG_DOM_BINARY && v != 0.0 && v != 1.0) config_error("binary dominance entries must be 0 or 1");
+    }
+}
+
+// ---- exact integer thresholds ------------------------------------------------------------------
+// r(x) = double(float(x) / 4294967295.0f) * total is monotone non-decreasing in the raw word x
+// (mt19937.hpp:62, engine.hpp:117), so every double comparison of the rule is a threshold on x.
+
+double r_of(uint32_t x, double total) { return static_cast<double>(static_cast<float>(x) / 4294967295.0f) * total; }
+
+// min{x in [lo, hi) : pred(x)} for a monotone predicate; hi when none.
+template <class Pred>
+uint64_t lower_bound_u32(uint64_t lo, uint64_t hi, Pred pred) {
+    while (lo < hi) {
+        const uint64_t mid = lo + (hi - lo) / 2;
+        if (pred(static_cast<uint32_t>(mid)))
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    return lo;
+}
+
+struct Thresholds {
+    uint32_t xm = 0, xi = 0;
+    std::vector<uint32_t> T;  // (S+1)^2
+};
+
+Thresholds compute_thresholds(double mobility, int64_t cells, const double* dom, int S) {
+    // action_rates (params.hpp:61-70)
+    const double mu = 1.0, sigma = 1.0, eps = 2.0 * mobility * static_cast<double>(cells);
+    const double total = mu + sigma + eps;
+    const double em = eps + mu;
+    Thresholds t;
+    const uint64_t xm = lower_bound_u32(0, uint64_t{1} << 32, [&](uint32_t x) { return r_of(x, total) >= eps; });
+    const uint64_t xi = lower_bound_u32(0, uint64_t{1} << 32, [&](uint32_t x) { return r_of(x, total) >= em; });
+    // r(2^32-1) = total >= eps + mu, so both exist.
+    t.xm = static_cast<uint32_t>(std::min<uint64_t>(xm, 0xFFFFFFFFull));
+    t.xi = static_cast<uint32_t>(std::min<uint64_t>(xi, 0xFFFFFFFFull));
+    const int S1 = S + 1;
+    t.T.assign(static_cast<size_t>(S1) * S1, t.xm);
+    for (int a = 1; a <= S; ++a) {
+        for (int b = 1; b <= S; ++b) {
+            const double d = dom[static_cast<size_t>(a - 1) * S + (b - 1)];
+            uint32_t T = t.xm;  // forward > 0.0 guard (engine.hpp:127,131): D == 0 never fires
+            if (d > 0.0) {
+                // u(x) = (r(x) - eps) / mu < d  ⇔  x < T  on [xm, xi)
+                const uint64_t v = lower_bound_u32(t.xm, t.xi, [&](uint32_t x) { return (r_of(x, total) - eps) / mu >= d; });
+                T = static_cast<uint32_t>(v);
+            }
+            t.T[static_cast<size_t>(a) * S1 + b] = T;
+        }
+    }
+    return t;
+}
+
+// min{x : double(float(x)/4294967295.0f) >= p0} — the empty test of init_lattice (lattice.hpp:59).
+uint32_t empty_threshold(double p0) {
+    if (!(p0 > 0.0)) return 0u;
+    const uint64_t v = lower_bound_u32(0, uint64_t{1} << 32, [&](uint32_t x) {
+        return static_cast<double>(static_cast<float>(x) / 4294967295.0f) >= p0;
+    });
+    return static_cast<uint32_t>(std::min<uint64_t>(v, 0xFFFFFFFFull));
+}
+
+int64_t align_num_randoms_or_throw(int64_t requested, int64_t cells) {
+    if (cells < 1) config_error("cell count must be positive");
+    if (requested < cells)
+        config_error("numRandoms (" + std::to_string(requested) + ") must be at least the cell count (" +
+                     std::to_string(cells) + ")");
+    return requested / cells * cells;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        if (count == 0) return;
+        CK(cudaMalloc(&p, sizeof(T) * count));
+        n = count;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { free(); }
+};
+
+}  // namespace
+
+struct escg_dev {
+    escg_params p{};
+    int S = 0, S1 = 0, kind = 0, arity = 4, flux = 1, H = 0, L = 0;
+    int64_t N = 0;
+    int device = 0;
+    int nrep = 1;
+    int kernel = ESCG_KERNEL_TILE;
+    int threads = 512;
+    int smem = 0;
+    int P = 0;
+    int nby = 1, nbx = 1;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    Thresholds th;
+    uint32_t x_empty = 0;
+    std::vector<uint64_t> seeds;
+    std::vector<int64_t> mcs;  // host mirror per replica
+    std::vector<int> cur;      // block path: buffer holding replica r's lattice
+    DevBuf<uint8_t> lat[2];
+    DevBuf<uint64_t> d_seeds, d_last;
+    DevBuf<uint32_t> d_T;
+    DevBuf<int64_t> d_mcs, d_nrec, d_tsteps;
+    DevBuf<int32_t> d_status;
+    DevBuf<uint64_t> d_tcounts;
+    DevBuf<unsigned long long> d_acc;
+    DevBuf<unsigned int> d_ticket;
+    DevBuf<int> d_rows, d_cols, d_bad;
+    DevBuf<int32_t> d_i32;
+    int64_t trace_cap = 0;
+    bool traced = false;
+    double last_ms = 0.0;
+    int64_t last_launches = 0;
+
+    ~escg_dev() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+namespace {
+
+// Block-kernel decomposition: row/col splits at multiples of 4 minimising waves x window area.
+void plan_blocks(escg_dev* h, int sms, int smem_cap) {
+    const int uy = h->H / 4, ux = h->L / 4;
+    double best = 1e300;
+    int bnby = 1, bnbx = 1;
+    const int M = escgd::kMargin;
+    for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
+        for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
+            const int bh = ((uy + nby - 1) / nby) * 4, bw = ((ux + nbx - 1) / nbx) * 4;
+            const int Pw = ((bw + 2 * M) + 15) & ~15;
+            const int bytes = (bh + 2 * M) * Pw + h->S1 * h->S1 * 4 + (escgd::kMaxSpecies + 1) * 4 + 64;
+            if (bytes > smem_cap) continue;
+            const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
+            const int64_t waves = (ctas + sms - 1) / sms;
+            // compute ∝ average valid area over the 4 phases (margin 12 → mean extra ~6 per side)
+            const double cost = static_cast<double>(waves) * (bh + 12.0) * (bw + 12.0) + 2000.0 * waves;
+            if (cost < best) {
+                best = cost;
+                bnby = nby;
+                bnbx = nbx;
+            }
+        }
+    }
+    h->nby = bnby;
+    h->nbx = bnbx;
+    std::vector<int> rows(bnby + 1), cols(bnbx + 1);
+    for (int i = 0; i <= bnby; ++i) rows[i] = static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
+    for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(ux) * i / bnbx) * 4;
+    int bh = 0, bw = 0;
+    for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
+    for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
+    h->P = ((bw + 2 * M) + 15) & ~15;
+    h->smem = (((bh + 2 * M) * h->P + 15) & ~15) + h->S1 * h->S1 * 4 + (escgd::kMaxSpecies + 1) * 4 + 64;
+    h->d_rows.alloc(rows.size());
+    h->d_cols.alloc(cols.size());
+    CK(cudaMemcpy(h->d_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_cols.p, cols.data(), sizeof(int) * cols.size(), cudaMemcpyHostToDevice));
+}
+
+escgd::RuleArgs rule_args(escg_dev* h) { return escgd::RuleArgs{h->th.xm, h->th.xi, h->d_T.p}; }
+
+escgd::RunArgs run_args(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int tracked, bool trace) {
+    escgd::RunArgs r{};
+    r.mcs = h->d_mcs.p;
+    r.status = h->d_status.p;
+    r.last_counts = h->d_last.p;
+    r.n_rec = h->d_nrec.p;
+    r.trace_steps = trace ? h->d_tsteps.p : nullptr;
+    r.trace_counts = trace ? h->d_tcounts.p : nullptr;
+    r.trace_cap = trace ? h->trace_cap : 0;
+    r.mcs_limit = limit;
+    r.interval = interval;
+    r.stop_flags = flags;
+    r.tracked = tracked;
+    return r;
+}
+
+void upload_mcs(escg_dev* h) {
+    CK(cudaMemcpyAsync(h->d_mcs.p, h->mcs.data(), sizeof(int64_t) * h->nrep, cudaMemcpyHostToDevice, h->stream));
+}
+
+// Block path: bring every replica's lattice into buffer 0 so one launch serves all replicas.
+void normalize_buffers(escg_dev* h) {
+    if (h->kernel != ESCG_KERNEL_BLOCK) return;
+    for (int r = 0; r < h->nrep; ++r) {
+        if (h->cur[r] != 0) {
+            CK(cudaMemcpyAsync(h->lat[0].p + static_cast<size_t>(r) * h->N, h->lat[1].p + static_cast<size_t>(r) * h->N,
+                               h->N, cudaMemcpyDeviceToDevice, h->stream));
+            h->cur[r] = 0;
+        }
+    }
+    for (int r = 1; r < h->nrep; ++r)
+        if (h->mcs[r] != h->mcs[0]) config_error("block kernel requires all replicas at the same MCS");
+}
+
+uint8_t* replica_lat(escg_dev* h, int r) {
+    return h->lat[h->kernel == ESCG_KERNEL_BLOCK ? h->cur[r] : 0].p + static_cast<size_t>(r) * h->N;
+}
+
+void check_replica(escg_dev* h, int r) {
+    if (r < 0 || r >= h->nrep) config_error("replica index out of range");
+}
+
+void timed_begin(escg_dev* h) { CK(cudaEventRecord(h->ev0, h->stream)); }
+void timed_end(escg_dev* h, int64_t launches) {
+    CK(cudaEventRecord(h->ev1, h->stream));
+    CK(cudaEventSynchronize(h->ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, h->ev0, h->ev1));
+    h->last_ms = ms;
+    h->last_launches = launches;
+}
+
+// Block path: enqueue MCS [t, t+n) with records at the end when `record_last`.
+int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, const escgd::RunArgs& run,
+                            int64_t t0) {
+    escgd::BlockArgs a{};
+    a.seeds = h->d_seeds.p;
+    a.rule = rule_args(h);
+    a.run = run;
+    a.H = h->H;
+    a.L = h->L;
+    a.S = h->S;
+    a.P = h->P;
+    a.arity = h->arity;
+    a.nby = h->nby;
+    a.nbx = h->nbx;
+    a.row_split = h->d_rows.p;
+    a.col_split = h->d_cols.p;
+    a.acc = h->d_acc.p;
+    a.ticket = h->d_ticket.p;
+    a.smem_bytes = h->smem;
+    a.step = 1;
+    for (int64_t k = 0; k < n; ++k) {
+        const int64_t m = t + k;
+        const int par = static_cast<int>((m - t0) & 1);
+        a.src = h->lat[par].p;
+        a.dst = h->lat[1 - par].p;
+        a.mcs = m;
+        a.count = (count_last && k == n - 1) ? 1 : 0;
+        CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
+    }
+    return n;
+}
+
+void ensure_trace(escg_dev* h, int64_t records) {
+    const int64_t cap = std::max<int64_t>(records, 1);
+    const double bytes = static_cast<double>(cap) * h->nrep * (h->S1 * 8 + 8);
+    if (bytes > 8e9) config_error("density trace too large for device memory; disable record_trace");
+    if (h->trace_cap < cap) {
+        h->d_tsteps.alloc(static_cast<size_t>(cap) * h->nrep);
+        h->d_tcounts.alloc(static_cast<size_t>(cap) * h->nrep * h->S1);
+        h->trace_cap = cap;
+    }
+}
+
+void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int tracked, bool trace,
+              int32_t* status_out) {
+    if (interval < 1) config_error("sample interval must be positive");
+    if (tracked < 0 || tracked > h->S) config_error("tracked species out of range");
+    normalize_buffers(h);
+    for (int r = 0; r < h->nrep; ++r)
+        if (h->mcs[r] > limit) config_error("run limit is below the current MCS");
+    int64_t span = 0;
+    for (int r = 0; r < h->nrep; ++r) span = std::max(span, limit - h->mcs[r]);
+    if (trace) ensure_trace(h, span / interval + 2);
+    h->traced = trace;
+    CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t) * h->nrep, h->stream));  // ESCG_RUNNING
+    CK(cudaMemsetAsync(h->d_nrec.p, 0, sizeof(int64_t) * h->nrep, h->stream));
+    upload_mcs(h);
+    const escgd::RunArgs run = run_args(h, limit, interval, flags, tracked, trace);
+    int64_t launches = 0;
+    timed_begin(h);
+    if (h->kernel == ESCG_KERNEL_TILE) {
+        escgd::TileArgs a{};
+        a.lat = h->lat[0].p;
+        a.seeds = h->d_seeds.p;
+        a.rule = rule_args(h);
+        a.run = run;
+        a.H = h->H;
+        a.L = h->L;
+        a.S = h->S;
+        a.P = h->P;
+        a.arity = h->arity;
+        a.flux = h->flux;
+        a.record = 1;
+        a.smem_bytes = h->smem;
+        CK(escgd::launch_tile(a, h->nrep, h->threads, h->stream));
+        launches = 1;
+    } else {
+        CK(cudaMemsetAsync(h->d_acc.p, 0, sizeof(unsigned long long) * h->S1 * h->nrep, h->stream));
+        CK(cudaMemsetAsync(h->d_ticket.p, 0, sizeof(unsigned int) * h->nrep, h->stream));
+        const int64_t t0 = h->mcs[0];
+        // record at the starting MCS (record_and_check before any step, engine.cpp:181)
+        escgd::BlockArgs a{};
+        a.src = h->lat[0].p;
+        a.dst = h->lat[1].p;
+        a.seeds = h->d_seeds.p;
+        a.rule = rule_args(h);
+        a.run = run;
+        a.H = h->H;
+        a.L = h->L;
+        a.S = h->S;
+        a.P = h->P;
+        a.arity = h->arity;
+        a.nby = h->nby;
+        a.nbx = h->nbx;
+        a.row_split = h->d_rows.p;
+        a.col_split = h->d_cols.p;
+        a.mcs = t0;
+        a.step = 0;
+        a.count = 1;
+        a.acc = h->d_acc.p;
+        a.ticket = h->d_ticket.p;
+        a.smem_bytes = h->smem;
+        CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
+        ++launches;
+        // Poll the device status every few chunks so a stasis/stop does not leave thousands of
+        // no-op launches queued; the poll lags one chunk behind the enqueue front.
+        int32_t* hstat = nullptr;
+        CK(cudaMallocHost(&hstat, sizeof(int32_t) * h->nrep));
+        cudaEvent_t polled = nullptr;
+        CK(cudaEventCreateWithFlags(&polled, cudaEventDisableTiming));
+        bool poll_pending = false;
+        int64_t t = t0, since_poll = 0;
+        const int64_t kChunk = 512;
+        while (t < limit) {
+            const int64_t adv = std::min(interval, limit - t);
+            launches += enqueue_block_steps(h, t, adv, true, run, t0);
+            t += adv;
+            since_poll += adv;
+            if (since_poll >= kChunk) {
+                since_poll = 0;
+                if (poll_pending) {
+                    CK(cudaEventSynchronize(polled));
+                    bool all_done = true;
+                    for (int r = 0; r < h->nrep; ++r) all_done &= hstat[r] != ESCG_RUNNING;
+                    if (all_done) break;
+                }
+                CK(cudaMemcpyAsync(hstat, h->d_status.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaEventRecord(polled, h->stream));
+                poll_pending = true;
+            }
+        }
+        cudaEventDestroy(polled);
+        cudaFreeHost(hstat);
+    }
+    timed_end(h, launches);
+    CK(cudaGetLastError());
+    std::vector<int32_t> st(h->nrep);
+    CK(cudaMemcpy(h->mcs.data(), h->d_mcs.p, sizeof(int64_t) * h->nrep, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(st.data(), h->d_status.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost));
+    if (status_out) std::memcpy(status_out, st.data(), sizeof(int32_t) * h->nrep);
+}
+
+}  // namespace
+
+// ================================== C ABI ======================================================
+
+extern "C" {
+
+const char* escg_dev_last_error(void) { return g_last_error.c_str(); }
+
+int escg_params_default(escg_params* out) {
+    return guarded([&] {
+        if (!out) config_error("null params");
+        escg_params p{};
+        p.length = 200;
+        p.height = 200;
+        p.mcs_limit = 100000;
+        p.neighbourhood = 4;
+        p.print_frequency = 200;
+        p.mobility = 3e-05;
+        p.species = 3;
+        p.flux = 1;
+        p.empty_prob = 0.0;
+        p.num_randoms = 100000000;
+        *out = p;
+    });
+}
+
+int escg_validate(const escg_params* p, const double* dominance, int32_t species, int32_t kind) {
+    return guarded([&] {
+        if (!p) config_error("null params");
+        validate_params(*p);
+        validate_dominance(dominance, species, kind);
+        if (species != p->species)
+            config_error("species count (" + std::to_string(p->species) + ") does not match dominance size (" +
+                         std::to_string(species) + ")");
+    });
+}
+
+int escg_action_rates(double mobility, int64_t cells, double* out4) {
+    return guarded([&] {
+        if (mobility < 0.0) config_error("mobility must be non-negative");
+        if (cells < 1) config_error("cell count must be positive");
+        out4[0] = 1.0;
+        out4[1] = 1.0;
+        out4[2] = 2.0 * mobility * static_cast<double>(cells);
+        out4[3] = out4[0] + out4[1] + out4[2];
+    });
+}
+
+int escg_thresholds(double mobility, int64_t cells, const double* dominance, int32_t species, uint32_t* out_xmx,
+                    uint32_t* out_T) {
+    return guarded([&] {
+        if (mobility < 0.0) config_error("mobility must be non-negative");
+        if (cells < 1) config_error("cell count must be positive");
+        Thresholds t = compute_thresholds(mobility, cells, dominance, species);
+        out_xmx[0] = t.xm;
+        out_xmx[1] = t.xi;
+        if (out_T) std::memcpy(out_T, t.T.data(), sizeof(uint32_t) * t.T.size());
+    });
+}
+
+int64_t escg_align_num_randoms(int64_t requested, int64_t cells) {
+    int64_t out = -1;
+    const int rc = guarded([&] { out = align_num_randoms_or_throw(requested, cells); });
+    return rc == ESCG_OK ? out : -1;
+}
+
+int escg_dev_create(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t device,
+                    int32_t n_replicas, const uint64_t* replica_seeds, int32_t kernel, escg_dev** out) {
+    return guarded([&] {
+        if (!p || !out) config_error("null argument");
+        *out = nullptr;
+        validate_params(*p);
+        validate_dominance(dominance, species, kind);
+        if (species != p->species)
+            config_error("species count (" + std::to_string(p->species) + ") does not match dominance size (" +
+                         std::to_string(species) + ")");
+        if (n_replicas < 1) config_error("replica count must be positive");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+            engine_error("no CUDA device available (the ESCG engine has no CPU fallback)");
+        if (device < 0 || device >= ndev) config_error("CUDA device index out of range");
+        CK(cudaSetDevice(device));
+        auto h = std::make_unique<escg_dev>();
+        h->p = *p;
+        h->S = species;
+        h->S1 = species + 1;
+        h->kind = kind;
+        h->arity = p->neighbourhood;
+        h->flux = p->flux ? 1 : 0;
+        h->H = p->height;
+        h->L = p->length;
+        h->N = static_cast<int64_t>(h->H) * h->L;
+        h->device = device;
+        h->nrep = n_replicas;
+        const uint64_t base_seed = p->has_seed ? p->seed : 0x5EEDull;
+        h->seeds.resize(n_replicas);
+        for (int r = 0; r < n_replicas; ++r) h->seeds[r] = replica_seeds ? replica_seeds[r] : base_seed + r;
+        h->th = compute_thresholds(p->mobility, h->N, dominance, species);
+        h->x_empty = empty_threshold(p->empty_prob);
+        h->mcs.assign(n_replicas, 0);
+        h->cur.assign(n_replicas, 0);
+
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        const int smem_cap = escgd::max_smem_optin(device);
+        int tpitch = 0;
+        const int tbytes = escgd::tile_smem_bytes(h->H, h->L, species, &tpitch);
+        const bool periodic4 = h->flux && (h->H % 4 == 0) && (h->L % 4 == 0);
+        if (h->flux && !periodic4)
+            config_error("device engine: periodic lattices need L and H divisible by 4 (2x2 tiles, 2 colours per axis)");
+        int choice = kernel;
+        if (choice == ESCG_KERNEL_AUTO) choice = tbytes <= smem_cap ? ESCG_KERNEL_TILE : ESCG_KERNEL_BLOCK;
+        if (choice == ESCG_KERNEL_TILE && tbytes > smem_cap)
+            config_error("lattice too large for the shared-memory tile kernel");
+        if (choice == ESCG_KERNEL_BLOCK && !periodic4)
+            config_error("block kernel supports periodic (flux) lattices only");
+        h->kernel = choice;
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&h->ev0));
+        CK(cudaEventCreate(&h->ev1));
+        h->lat[0].alloc(static_cast<size_t>(h->N) * n_replicas);
+        if (choice == ESCG_KERNEL_TILE) {
+            h->P = tpitch;
+            h->smem = tbytes;
+            h->threads = 512;
+        } else {
+            h->lat[1].alloc(static_cast<size_t>(h->N) * n_replicas);
+            plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024));
+            h->threads = 1024;
+            h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
+            h->d_ticket.alloc(n_replicas);
+        }
+        h->d_seeds.alloc(n_replicas);
+        h->d_last.alloc(static_cast<size_t>(h->S1) * n_replicas);
+        h->d_T.alloc(h->th.T.size());
+        h->d_mcs.alloc(n_replicas);
+        h->d_nrec.alloc(n_replicas);
+        h->d_status.alloc(n_replicas);
+        h->d_bad.alloc(1);
+        CK(cudaMemcpy(h->d_seeds.p, h->seeds.data(), sizeof(uint64_t) * n_replicas, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(h->d_T.p, h->th.T.data(), sizeof(uint32_t) * h->th.T.size(), cudaMemcpyHostToDevice));
+        CK(cudaMemset(h->lat[0].p, 0, static_cast<size_t>(h->N) * n_replicas));
+        CK(cudaMemset(h->d_status.p, 0xFF, sizeof(int32_t) * n_replicas));
+        CK(cudaMemset(h->d_nrec.p, 0, sizeof(int64_t) * n_replicas));
+        CK(cudaMemset(h->d_last.p, 0, sizeof(uint64_t) * h->S1 * n_replicas));
+        *out = h.release();
+    });
+}
+
+int escg_dev_destroy(escg_dev* h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaSetDevice(h->device);
+        delete h;
+    });
+}
+
+int escg_dev_init_lattice(escg_dev* h) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        CK(cudaSetDevice(h->device));
+        escgd::InitArgs a{};
+        a.lat = h->lat[0].p;
+        a.seeds = h->d_seeds.p;
+        a.n = h->N;
+        a.nrep = h->nrep;
+        a.S = h->S;
+        a.x_empty = h->x_empty;
+        a.all_empty = h->p.empty_prob >= 1.0 ? 1 : 0;
+        CK(escgd::launch_init(a, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        std::fill(h->mcs.begin(), h->mcs.end(), 0);
+        std::fill(h->cur.begin(), h->cur.end(), 0);
+    });
+}
+
+int escg_dev_set_lattice(escg_dev* h, int32_t replica, const int32_t* cells, int64_t mcs) {
+    return guarded([&] {
+        if (!h || !cells) config_error("null argument");
+        check_replica(h, replica);
+        if (mcs < 0) config_error("mcs must be non-negative");
+        CK(cudaSetDevice(h->device));
+        if (h->d_i32.n < static_cast<size_t>(h->N)) h->d_i32.alloc(h->N);
+        CK(cudaMemcpyAsync(h->d_i32.p, cells, sizeof(int32_t) * h->N, cudaMemcpyHostToDevice, h->stream));
+        CK(cudaMemsetAsync(h->d_bad.p, 0, sizeof(int), h->stream));
+        CK(escgd::launch_i32_to_u8(h->d_i32.p, replica_lat(h, replica), h->N, h->S, h->d_bad.p, h->stream));
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, h->d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (bad) throw Error(ESCG_EENGINE, "corrupt lattice value (outside [0, S])");
+        h->mcs[replica] = mcs;
+    });
+}
+
+int escg_dev_get_lattice(escg_dev* h, int32_t replica, int32_t* out, int64_t* mcs_out) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        check_replica(h, replica);
+        CK(cudaSetDevice(h->device));
+        if (out) {
+            if (h->d_i32.n < static_cast<size_t>(h->N)) h->d_i32.alloc(h->N);
+            CK(escgd::launch_u8_to_i32(replica_lat(h, replica), h->d_i32.p, h->N, h->stream));
+            CK(cudaMemcpyAsync(out, h->d_i32.p, sizeof(int32_t) * h->N, cudaMemcpyDeviceToHost, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        if (mcs_out) *mcs_out = h->mcs[replica];
+    });
+}
+
+int escg_dev_counts(escg_dev* h, int32_t replica, uint64_t* out) {
+    return guarded([&] {
+        if (!h || !out) config_error("null argument");
+        check_replica(h, replica);
+        CK(cudaSetDevice(h->device));
+        DevBuf<unsigned long long> tmp;
+        tmp.alloc(h->S1);
+        CK(escgd::launch_count(replica_lat(h, replica), h->N, 1, h->S, tmp.p, h->stream));
+        CK(cudaMemcpyAsync(out, tmp.p, sizeof(uint64_t) * h->S1, cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+    });
+}
+
+int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (n_mcs < 0) config_error("mcs count must be non-negative");
+        CK(cudaSetDevice(h->device));
+        normalize_buffers(h);
+        int64_t launches = 0;
+        if (h->kernel == ESCG_KERNEL_TILE) {
+            upload_mcs(h);
+            escgd::TileArgs a{};
+            a.lat = h->lat[0].p;
+            a.seeds = h->d_seeds.p;
+            a.rule = rule_args(h);
+            a.run = run_args(h, 0, 1, 0, 0, false);
+            a.H = h->H;
+            a.L = h->L;
+            a.S = h->S;
+            a.P = h->P;
+            a.arity = h->arity;
+            a.flux = h->flux;
+            a.record = 0;
+            a.smem_bytes = h->smem;
+            // per-replica limit: all replicas advance by n_mcs from their own MCS; the kernel
+            // reads mcs[r] and runs to mcs_limit, so stage limit = mcs + n per replica by
+            // shifting: launch once per distinct starting MCS.
+            std::vector<int64_t> starts(h->mcs);
+            std::sort(starts.begin(), starts.end());
+            starts.erase(std::unique(starts.begin(), starts.end()), starts.end());
+            if (starts.size() != 1) config_error("advance requires all replicas at the same MCS");
+            a.run.mcs_limit = starts[0] + n_mcs;
+            timed_begin(h);
+            CK(escgd::launch_tile(a, h->nrep, h->threads, h->stream));
+            launches = 1;
+            timed_end(h, launches);
+            for (auto& m : h->mcs) m += n_mcs;
+        } else {
+            const escgd::RunArgs run = run_args(h, 0, 1, 0, 0, false);
+            CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t) * h->nrep, h->stream));
+            const int64_t t0 = h->mcs[0];
+            timed_begin(h);
+            launches = enqueue_block_steps(h, t0, n_mcs, false, run, t0);
+            timed_end(h, launches);
+            for (int r = 0; r < h->nrep; ++r) {
+                h->mcs[r] += n_mcs;
+                h->cur[r] = static_cast<int>(n_mcs & 1);
+            }
+        }
+        CK(cudaGetLastError());
+    });
+}
+
+int escg_dev_run(escg_dev* h, int64_t mcs_limit, int64_t interval, uint32_t stop_flags, int32_t tracked_species,
+                 int32_t record_trace, int32_t* status_out) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        CK(cudaSetDevice(h->device));
+        const std::vector<int64_t> start(h->mcs);
+        run_impl(h, mcs_limit, interval, stop_flags, tracked_species, record_trace != 0, status_out);
+        if (h->kernel == ESCG_KERNEL_BLOCK)
+            for (int r = 0; r < h->nrep; ++r) h->cur[r] = static_cast<int>((h->mcs[r] - start[r]) & 1);
+    });
+}
+
+int escg_dev_read_trace(escg_dev* h, int32_t replica, int64_t* steps, uint64_t* counts, int64_t cap, int64_t* n_out) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        check_replica(h, replica);
+        CK(cudaSetDevice(h->device));
+        int64_t n = 0;
+        CK(cudaMemcpy(&n, h->d_nrec.p + replica, sizeof(int64_t), cudaMemcpyDeviceToHost));
+        if (n_out) *n_out = n;
+        if (!h->traced) return;
+        const int64_t m = std::min({n, cap, h->trace_cap});
+        if (m <= 0) return;
+        if (steps)
+            CK(cudaMemcpy(steps, h->d_tsteps.p + static_cast<size_t>(replica) * h->trace_cap, sizeof(int64_t) * m,
+                          cudaMemcpyDeviceToHost));
+        if (counts)
+            CK(cudaMemcpy(counts, h->d_tcounts.p + static_cast<size_t>(replica) * h->trace_cap * h->S1,
+                          sizeof(uint64_t) * m * h->S1, cudaMemcpyDeviceToHost));
+    });
+}
+
+int escg_dev_replica_result(escg_dev* h, int32_t replica, int64_t* mcs, int32_t* status, uint64_t* last_counts) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        check_replica(h, replica);
+        CK(cudaSetDevice(h->device));
+        if (mcs) *mcs = h->mcs[replica];
+        if (status) CK(cudaMemcpy(status, h->d_status.p + replica, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (last_counts)
+            CK(cudaMemcpy(last_counts, h->d_last.p + static_cast<size_t>(replica) * h->S1, sizeof(uint64_t) * h->S1,
+                          cudaMemcpyDeviceToHost));
+    });
+}
+
+int escg_dev_replay(escg_dev* h, const uint32_t* w_cell, const uint32_t* w_dir, const uint32_t* w_act, int64_t n) {
+    return guarded([&] {
+        if (!h || !w_cell || !w_dir || !w_act) config_error("null argument");
+        if (n < 0) config_error("attempt count must be non-negative");
+        CK(cudaSetDevice(h->device));
+        DevBuf<uint32_t> wc, wd, wa;
+        wc.alloc(std::max<int64_t>(n, 1));
+        wd.alloc(std::max<int64_t>(n, 1));
+        wa.alloc(std::max<int64_t>(n, 1));
+        CK(cudaMemcpy(wc.p, w_cell, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(wd.p, w_dir, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(wa.p, w_act, sizeof(uint32_t) * n, cudaMemcpyHostToDevice));
+        escgd::ReplayArgs a{};
+        a.lat = replica_lat(h, 0);
+        a.wc = wc.p;
+        a.wd = wd.p;
+        a.wa = wa.p;
+        a.n_attempts = n;
+        a.rule = rule_args(h);
+        a.H = h->H;
+        a.L = h->L;
+        a.S = h->S;
+        a.arity = h->arity;
+        a.flux = h->flux;
+        timed_begin(h);
+        CK(escgd::launch_replay(a, h->stream));
+        timed_end(h, 1);
+    });
+}
+
+int escg_dev_last_timing(escg_dev* h, double* ms, int64_t* launches) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (ms) *ms = h->last_ms;
+        if (launches) *launches = h->last_launches;
+    });
+}
+
+int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t* threads, int32_t* smem_bytes) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (kernel) *kernel = h->kernel;
+        if (grid_ctas) *grid_ctas = h->kernel == ESCG_KERNEL_TILE ? h->nrep : h->nby * h->nbx * h->nrep;
+        if (threads) *threads = h->threads;
+        if (smem_bytes) *smem_bytes = h->smem;
+    });
+}
+
+int escg_simulate(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t mode,
+                  int32_t device, const int32_t* resume_cells, int64_t resume_mcs, uint32_t stop_flags,
+                  int32_t tracked_species, int32_t* out_cells, int64_t* out_mcs, int64_t* steps, uint64_t* counts,
+                  int64_t cap, int64_t* n_records, int32_t* status) {
+    return guarded([&] {
+        if (!p) config_error("null params");
+        validate_params(*p);
+        const int64_t N = static_cast<int64_t>(p->length) * p->height;
+        int64_t interval = 1;
+        if (mode == ESCG_MODE_MAX_STEP) interval = align_num_randoms_or_throw(p->num_randoms, N) / N;
+        else if (mode == ESCG_MODE_PARALLEL_MCS) align_num_randoms_or_throw(p->num_randoms, N);  // engine.cpp:142
+        else if (mode != ESCG_MODE_SERIAL) config_error("unknown engine mode");
+        // Engines are cached per thread by shape/model so repeated calls reuse device buffers.
+        struct Cache {
+            escg_dev* h = nullptr;
+            std::vector<double> dom;
+            escg_params p{};
+            int kind = -1, device = -1;
+            ~Cache() {
+                if (h) escg_dev_destroy(h);
+            }
+        };
+        thread_local Cache cache;
+        std::vector<double> dom(dominance, dominance + static_cast<size_t>(species) * species);
+        escg_params key = *p;
+        const bool same = cache.h && cache.kind == kind && cache.device == device && cache.dom == dom &&
+                          std::memcmp(&cache.p, &key, sizeof(escg_params)) == 0;
+        if (!same) {
+            if (cache.h) escg_dev_destroy(cache.h);
+            cache.h = nullptr;
+            escg_dev* h = nullptr;
+            const int rc = escg_dev_create(p, dominance, species, kind, device, 1, nullptr, ESCG_KERNEL_AUTO, &h);
+            if (rc != ESCG_OK) throw Error(rc, g_last_error);
+            cache.h = h;
+            cache.dom = dom;
+            cache.p = key;
+            cache.kind = kind;
+            cache.device = device;
+        }
+        escg_dev* h = cache.h;
+        int rc;
+        if (resume_cells)
+            rc = escg_dev_set_lattice(h, 0, resume_cells, resume_mcs);
+        else
+            rc = escg_dev_init_lattice(h);
+        if (rc != ESCG_OK) throw Error(rc, g_last_error);
+        const uint32_t flags = stop_flags | ESCG_STOP_STASIS | (tracked_species >= 1 ? ESCG_STOP_TRACKED : 0u);
+        int32_t st = 0;
+        rc = escg_dev_run(h, p->mcs_limit, interval, flags, tracked_species, (steps || counts) ? 1 : 0, &st);
+        if (rc != ESCG_OK) throw Error(rc, g_last_error);
+        int64_t n = 0;
+        rc = escg_dev_read_trace(h, 0, steps, counts, cap, &n);
+        if (rc != ESCG_OK) throw Error(rc, g_last_error);
+        if (n_records) *n_records = n;
+        rc = escg_dev_get_lattice(h, 0, out_cells, out_mcs);
+        if (rc != ESCG_OK) throw Error(rc, g_last_error);
+        if (status) *status = st;
+    });
+}
+
+}  // extern "C"

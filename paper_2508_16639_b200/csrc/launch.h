@@ -1,0 +1,98 @@
+// launch.h — argument blocks and launchers shared by the host engine (engine.cpp) and the
+// sm_100a kernels (kernels.cu).  No torch types; plain device pointers.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace escgd {
+
+// Margin of the overlapped-tile (block) kernel: a tile footprint reaches 3 cells past the tile
+// origin, so validity shrinks by 3 cells per phase and 4 phases need 12 cells.
+constexpr int kMargin = 12;
+// Tile-kernel window: rows -2..H, cols -2..L (ghost frame of the periodic wrap), origin (2, 4).
+constexpr int kTileR0 = 2;
+constexpr int kTileC0 = 4;
+constexpr int kMaxSpecies = 64;
+
+struct RuleArgs {
+    uint32_t xm, xi;       // X_mig, X_int
+    const uint32_t* T;     // (S+1)^2 interaction thresholds (device)
+};
+
+// Per-replica run bookkeeping (device arrays, length n_replicas unless noted).
+struct RunArgs {
+    int64_t* mcs;             // current MCS
+    int32_t* status;          // ESCG_RUNNING (-1) or final RunStatus
+    uint64_t* last_counts;    // [rep][S+1] last density record
+    int64_t* n_rec;           // records written this run
+    int64_t* trace_steps;     // [rep][cap] or nullptr
+    uint64_t* trace_counts;   // [rep][cap][S+1] or nullptr
+    int64_t trace_cap;
+    int64_t mcs_limit;
+    int64_t interval;
+    uint32_t stop_flags;
+    int32_t tracked;
+};
+
+struct TileArgs {
+    uint8_t* lat;  // [rep][H*L], row-major
+    const uint64_t* seeds;
+    RuleArgs rule;
+    RunArgs run;
+    int H, L, S, P;   // P = shared-memory pitch
+    int arity, flux;
+    int record;       // 1: record/check loop (escg_dev_run); 0: advance to run.mcs_limit
+    int smem_bytes;
+};
+
+struct BlockArgs {
+    const uint8_t* src;  // [rep][H*L]
+    uint8_t* dst;
+    const uint64_t* seeds;
+    RuleArgs rule;
+    RunArgs run;
+    int H, L, S, P;      // P = window pitch
+    int arity;
+    int nby, nbx;
+    const int* row_split;  // nby+1 row boundaries (multiples of 4)
+    const int* col_split;  // nbx+1
+    int64_t mcs;           // MCS executed by this launch
+    int step;              // 1: execute MCS `mcs` (src → dst); 0: count src only
+    int count;             // 1: record densities of the result (at mcs+step)
+    unsigned long long* acc;  // [rep][S+1] cross-CTA accumulators (zero between records)
+    unsigned int* ticket;     // [rep]
+    int smem_bytes;
+};
+
+struct InitArgs {
+    uint8_t* lat;
+    const uint64_t* seeds;
+    int64_t n;          // cells per replica
+    int nrep;
+    int S;
+    uint32_t x_empty;   // cell empty iff first word < x_empty (empty_prob test, lattice.hpp:59)
+    int all_empty;      // empty_prob >= 1 (lattice.hpp:56-57)
+};
+
+struct ReplayArgs {
+    uint8_t* lat;
+    const uint32_t* wc;
+    const uint32_t* wd;
+    const uint32_t* wa;
+    int64_t n_attempts;
+    RuleArgs rule;
+    int H, L, S, arity, flux;
+};
+
+cudaError_t launch_init(const InitArgs& a, cudaStream_t s);
+cudaError_t launch_count(const uint8_t* lat, int64_t n, int nrep, int S, unsigned long long* out, cudaStream_t s);
+cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s);
+cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t s);
+cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
+cudaError_t launch_u8_to_i32(const uint8_t* src, int32_t* dst, int64_t n, cudaStream_t s);
+cudaError_t launch_i32_to_u8(const int32_t* src, uint8_t* dst, int64_t n, int S, int* bad, cudaStream_t s);
+int tile_smem_bytes(int H, int L, int S, int* pitch);
+int max_smem_optin(int device);
+
+}  // namespace escgd

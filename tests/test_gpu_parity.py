@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, bit-exact.
+
+1. Serial replay of injected reference MT19937 draws == reference run_serial (north_star clause
+   "given an injected identical random draw sequence ... bit-exact against the reference").
+2. Coloured schedule (tile and block kernels) == oracle/escg_oracle.c:orc_crs_run, which applies
+   the same Philox draws through the reference's double-precision elementary_step.
+3. Device init == oracle crs_init; fused density records == densities() of the exported lattice.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # L, H, S, M, p0, arity, flux, model
+    (8, 8, 3, 1e-4, 0.0, 4, True, "rps"),
+    (64, 64, 3, 1e-4, 0.1, 4, True, "rps"),
+    (48, 32, 5, 3e-5, 0.0, 4, True, "rpsls"),
+    (40, 40, 5, 3e-3, 0.2, 8, True, "ablated"),
+    (30, 22, 8, 0.0, 0.0, 4, False, "park8"),
+    (21, 35, 3, 1e-3, 0.1, 8, False, "rps"),
+]
+
+
+def model_of(escg, name):
+    return {
+        "rps": lambda: escg.make_circulant(3, [1]),
+        "rpsls": escg.make_rpsls,
+        "ablated": escg.make_rpsls_ablated,
+        "park8": lambda: escg.make_park8(0.15, 0.75, 1.0),
+    }[name]()
+
+
+def params(escg, L, H, S, M, p0, arity, flux, seed=1, mcs=100):
+    return escg.SimParams(length=L, height=H, species=S, mobility=M, empty_prob=p0,
+                          neighbourhood=escg.Neighbourhood(arity), flux=flux, seed=seed, mcs_limit=mcs)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}x{c[1]}_{c[7]}_n{c[5]}_{'flux' if c[6] else 'refl'}" for c in CASES])
+def test_replay_matches_reference_serial(escg, oracle, ref, case):
+    L, H, S, M, p0, arity, flux, name = case
+    model = model_of(escg, name)
+    seed, n_mcs = 11, 5
+    n = L * H * n_mcs
+    init, wc, wd, wa = oracle.serial_draws(L, H, S, p0, seed, n)
+    # the injected draws are exactly the reference's own stream (random_batch.hpp:44-53)
+    assert np.array_equal(init, ref.init_lattice(L, H, S, p0, seed))
+    expect = oracle.apply_draws(init, L, H, model.matrix(), M, wc, wd, wa, arity=arity, flux=flux)
+    if flux and arity == 4 and name == "rps":
+        got_ref = ref.simulate(L, H, model.matrix(), M, p0, n_mcs, seed, arity=arity, flux=flux)["cells"]
+        assert np.array_equal(expect, got_ref)
+    with escg.DeviceEngine(params(escg, L, H, S, M, p0, arity, flux), model, kernel="tile" if L * H < 40000 else "auto") as eng:
+        eng.set_lattice(init)
+        eng.replay(wc, wd, wa)
+        got = eng.get_lattice()
+    assert np.array_equal(got, expect)
+
+
+@pytest.mark.parametrize("name,eps", [("rps", 8.0), ("park8", 0.0), ("ablated", 60.0), ("rps", 2048.0),
+                                      ("rps", 53687.0912), ("park8", 3.0)])
+def test_replay_threshold_edges(escg, oracle, name, eps):
+    """One injected attempt per (s, n) pair per action word at every threshold X-1, X, X+1
+    (bucket edges and every interaction edge), all applied in a single device replay."""
+    model = model_of(escg, name)
+    S = model.size
+    L, H0 = 300, 8
+    # thresholds depend on (M, N) only through eps = 2MN; pick M for the target eps
+    probe_N = L * H0
+    xm, xi, T = escg.thresholds(eps / (2 * probe_N), probe_N, model)
+    edges = sorted({int(v) + d for v in [xm, xi, *T.ravel().tolist()] for d in (-1, 0, 1) if 0 <= int(v) + d < 2 ** 32})
+    edges += [0, 2 ** 32 - 1]
+    pairs = [(s, nb, x) for s in range(S + 1) for nb in range(S + 1) for x in edges]
+    H = max(4, -(-3 * len(pairs) // L))
+    H += (-H) % 4
+    N = L * H
+    M = eps / (2 * N)
+    rng = np.random.default_rng(5)
+    lat = rng.integers(0, S + 1, N).astype(np.int32)
+    wc = np.zeros(len(pairs), np.uint32)
+    wd = np.full(len(pairs), 3, np.uint32)  # right neighbour
+    wa = np.zeros(len(pairs), np.uint32)
+    for k, (s, nb, x) in enumerate(pairs):
+        c = 3 * k
+        lat[c], lat[c + 1] = s, nb
+        wc[k], wa[k] = c, x
+    want = oracle.apply_draws(lat, L, H, model.matrix(), M, wc, wd, wa)
+    with escg.DeviceEngine(params(escg, L, H, S, M, 0.0, 4, True), model, kernel="block") as eng:
+        eng.set_lattice(lat)
+        eng.replay(wc, wd, wa)
+        got = eng.get_lattice()
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, [pairs[i // 3] for i in bad[:5]]
+
+
+CRS_CASES = [
+    (8, 8, 3, 1e-4, 0.1, 4, True, "rps"),
+    (64, 48, 3, 1e-4, 0.1, 4, True, "rps"),
+    (100, 100, 5, 3e-5, 0.0, 4, True, "rpsls"),
+    (40, 36, 5, 3e-3, 0.2, 8, True, "ablated"),
+    (30, 22, 8, 0.0, 0.0, 4, False, "park8"),
+    (21, 35, 3, 1e-3, 0.1, 8, False, "rps"),
+    (13, 6, 3, 1e-2, 0.3, 4, False, "rps"),
+]
+
+
+@pytest.mark.parametrize("case", CRS_CASES, ids=[f"{c[0]}x{c[1]}_{c[7]}_n{c[5]}_{'flux' if c[6] else 'refl'}" for c in CRS_CASES])
+def test_tile_kernel_matches_crs_oracle(escg, oracle, case):
+    L, H, S, M, p0, arity, flux, name = case
+    model = model_of(escg, name)
+    seed = 0x1234567890AB
+    p = params(escg, L, H, S, M, p0, arity, flux, seed=seed)
+    with escg.DeviceEngine(p, model, kernel="tile") as eng:
+        eng.init_lattice()
+        init = eng.get_lattice()
+        assert np.array_equal(init, oracle.crs_init(L, H, S, p0, seed))
+        eng.advance(3)
+        got3 = eng.get_lattice()
+        eng.advance(4)
+        got7 = eng.get_lattice()
+    want3 = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 3, arity=arity, flux=flux)
+    assert np.array_equal(got3, want3)
+    want7 = oracle.crs_run(want3, L, H, model.matrix(), M, seed, 3, 4, arity=arity, flux=flux)
+    assert np.array_equal(got7, want7)
+
+
+@pytest.mark.parametrize("LH", [(64, 64), (200, 200), (96, 160), (8, 8)])
+@pytest.mark.parametrize("arity", [4, 8])
+def test_block_kernel_matches_crs_oracle(escg, oracle, LH, arity):
+    L, H = LH
+    model = escg.make_circulant(3, [1])
+    seed = 99
+    p = params(escg, L, H, 3, 1e-3, 0.1, arity, True, seed=seed)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(5)
+        got = eng.get_lattice()
+    want = oracle.crs_run(init, L, H, model.matrix(), 1e-3, seed, 0, 5, arity=arity)
+    assert np.array_equal(got, want)
+
+
+def test_block_equals_tile_kernel(escg):
+    L = 200
+    model = escg.make_rpsls()
+    p = params(escg, L, L, 5, 3e-5, 0.0, 4, True, seed=2024)
+    outs = []
+    for kernel in ("tile", "block"):
+        with escg.DeviceEngine(p, model, kernel=kernel) as eng:
+            eng.init_lattice()
+            eng.advance(40)
+            outs.append(eng.get_lattice())
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("kernel", ["tile", "block"])
+def test_run_records_and_stop_rules(escg, oracle, kernel):
+    """escg_dev_run: records at the reference cadence, counts == densities(), status rules."""
+    L = 64
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, L, 3, 1e-4, 0.1, 4, True, seed=5, mcs=23)
+    with escg.DeviceEngine(p, model, kernel=kernel) as eng:
+        eng.init_lattice()
+        init = eng.get_lattice()
+        st = eng.run(23, interval=5)
+        steps, counts = eng.read_trace()
+        final = eng.get_lattice()
+        assert st[0] == escg.RunStatus.Completed
+        assert steps.tolist() == [0, 5, 10, 15, 20, 23]
+        assert eng.mcs() == 23
+    want = oracle.crs_run(init, L, L, model.matrix(), 1e-4, 5, 0, 23)
+    assert np.array_equal(final, want)
+    assert np.array_equal(counts[-1], oracle.densities(want, 3))
+    assert np.array_equal(counts[0], oracle.densities(init, 3))
+
+
+def test_tracked_extinction_stops_like_on_record(escg, oracle):
+    """Ablated RPSLS: stop at the first record where Paper (4) is extinct (experiments.cpp:107-113)."""
+    L = 48
+    model = escg.make_rpsls_ablated()
+    p = params(escg, L, L, 5, 3e-5, 0.0, 4, True, seed=3, mcs=3000)
+    with escg.DeviceEngine(p, model, kernel="tile") as eng:
+        eng.init_lattice()
+        init = eng.get_lattice()
+        st = eng.run(3000, interval=1, tracked=4)
+        steps, counts = eng.read_trace()
+        t = eng.mcs()
+        final = eng.get_lattice()
+    assert st[0] == escg.RunStatus.Stopped
+    assert counts[-1][4] == 0 and all(c[4] > 0 for c in counts[:-1])
+    assert steps[-1] == t
+    assert np.array_equal(final, oracle.crs_run(init, L, L, model.matrix(), 3e-5, 3, 0, t))
+
+
+def test_replicas_equal_single_runs(escg):
+    L = 32
+    model = escg.make_circulant(3, [1])
+    seeds = [7, 8, 9, 10]
+    p = params(escg, L, L, 3, 1e-3, 0.1, 4, True)
+    with escg.DeviceEngine(p, model, n_replicas=4, seeds=seeds, kernel="tile") as eng:
+        eng.init_lattice()
+        eng.advance(50)
+        batch = [eng.get_lattice(r) for r in range(4)]
+    for r, s in enumerate(seeds):
+        p1 = params(escg, L, L, 3, 1e-3, 0.1, 4, True, seed=s)
+        with escg.DeviceEngine(p1, model, kernel="block") as eng:
+            eng.init_lattice()
+            eng.advance(50)
+            assert np.array_equal(eng.get_lattice(), batch[r])
+
+
+def test_simulate_one_call_matches_handle_path(escg, oracle):
+    L = 64
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, L, 3, 1e-4, 0.1, 4, True, seed=77, mcs=40)
+    res = escg.simulate(p, model, escg.EngineMode.ParallelMcs)
+    assert res.status == escg.RunStatus.Completed and res.state.current_mcs == 40
+    assert len(res.state.trace.steps) == 41
+    init = oracle.crs_init(L, L, 3, 0.1, 77)
+    want = oracle.crs_run(init, L, L, model.matrix(), 1e-4, 77, 0, 40)
+    assert np.array_equal(res.state.lattice.cells, want)
+    # hooks path (host-driven record_and_check) gives the same trajectory
+    seen = []
+    res2 = escg.simulate(p, model, escg.EngineMode.ParallelMcs,
+                         hooks=escg.RunHooks(on_record=lambda st: seen.append(st.current_mcs) or True))
+    assert seen == list(range(41))
+    assert np.array_equal(res2.state.lattice.cells, want)
