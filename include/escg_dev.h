@@ -146,6 +146,10 @@ ESCG_API int escg_dev_last_timing(escg_dev* h, double* ms, int64_t* launches);
 /* Kernel actually selected (ESCG_KERNEL_TILE / ESCG_KERNEL_BLOCK) and its launch geometry. */
 ESCG_API int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t* threads, int32_t* smem_bytes);
 
+/* Draw format chosen for this engine: 0 WIDE (32-bit attempt words), 1 NARROW (16-bit words, one
+ * draw per tile pair) — DESIGN.md §RNG; the oracle needs it to replay the schedule. */
+ESCG_API int escg_dev_draw_format(escg_dev* h, int32_t* narrow);
+
 /* One-call mirror of escg::simulate(params, model, mode, …) (engine.cpp:194-240) for a single
  * lattice: initialise on device (or resume from resume_cells at resume_mcs), run to completion
  * under `mode`'s record cadence with the device stop predicates, return the final int32 lattice,

@@ -392,17 +392,28 @@ EXPORT void orc_philox(const uint32_t* ctr_in, const uint32_t* key_in, uint32_t*
     out[3] = c3;
 }
 
-/* Counter domains of the device schedule.  key = (seed_lo, seed_hi). */
+/* Draw spec of the device schedule, version 2:
+ *   key  = (0xA4093822, 0x299F31D0)  (fixed: round keys become immediates on the device)
+ *   c0   = tile id | tile-pair id | cell pair | 0  (by domain)
+ *   c1   = mcs bits 0..31
+ *   c2   = mcs bits 32..47 | domain << 16 | phase << 20 | attempt << 24
+ *   c3   = seed32 = u32(seed) ^ murmur_finalize(u32(seed >> 32))  (= u32(seed) for seeds < 2^32) */
 enum { DOM_STEP = 0, DOM_REFINE = 1, DOM_ROUND = 2, DOM_INIT = 3 };
+static const uint32_t kKey0 = 0xA4093822u, kKey1 = 0x299F31D0u;
 
-static void crs_draw(uint64_t seed, uint32_t c0, uint64_t mcs, uint32_t low, uint32_t* out) {
+EXPORT uint32_t orc_seed32(uint64_t seed) {
+    return (uint32_t)seed ^ orc_murmur_finalize((uint32_t)(seed >> 32));
+}
+
+static void crs_draw(uint64_t seed, uint32_t c0, uint64_t mcs, uint32_t dom, uint32_t phase, uint32_t attempt,
+                     uint32_t* out) {
     uint32_t ctr[4], key[2];
     ctr[0] = c0;
     ctr[1] = (uint32_t)mcs;
-    ctr[2] = ((uint32_t)((mcs >> 32) & 0xFFFFu) << 16) | low;
-    ctr[3] = 0;
-    key[0] = (uint32_t)seed;
-    key[1] = (uint32_t)(seed >> 32);
+    ctr[2] = ((uint32_t)(mcs >> 32) & 0xFFFFu) | (dom << 16) | (phase << 20) | (attempt << 24);
+    ctr[3] = orc_seed32(seed);
+    key[0] = kKey0;
+    key[1] = kKey1;
     orc_philox(ctr, key, out);
 }
 
@@ -415,7 +426,7 @@ static const uint8_t kPerm[24][4] = {
 /* Round parameters of MCS `mcs`: tiling origin (oy, ox) ∈ {0,1}² and the colour order. */
 EXPORT void orc_crs_round(uint64_t seed, uint64_t mcs, int* oy, int* ox, int* perm) {
     uint32_t w[4];
-    crs_draw(seed, 0u, mcs, (uint32_t)DOM_ROUND << 8, w);
+    crs_draw(seed, 0u, mcs, DOM_ROUND, 0, 0, w);
     *oy = (int)(w[0] & 1u);
     *ox = (int)((w[0] >> 1) & 1u);
     const uint32_t pi = (uint32_t)(((uint64_t)w[1] * 24u) >> 32);
@@ -433,11 +444,34 @@ EXPORT void orc_crs_init(int length, int height, int species, double empty_prob,
     for (int64_t i = 0; i < n; ++i) {
         cells[i] = 0;
         if (empty_prob >= 1.0) continue;
-        crs_draw(seed, (uint32_t)(i >> 1), 0, (uint32_t)DOM_INIT << 8, w);
+        crs_draw(seed, (uint32_t)(i >> 1), 0, DOM_INIT, 0, 0, w);
         const uint32_t we = (i & 1) ? w[2] : w[0];
         const uint32_t ws = (i & 1) ? w[3] : w[1];
         if (empty_prob > 0.0 && (double)orc_unit(we) < empty_prob) continue;
         cells[i] = (int32_t)(ws % (uint32_t)species) + 1;
+    }
+}
+
+/* Draw formats.  LB = direction bits + 2 (cell bits) = 4 (VN4) / 5 (Moore8).
+ *  WIDE   one STEP draw per 2x2 tile (c0 = tile id); attempt a uses 32-bit word a:
+ *         bits [0,LB) direction/cell, action x = (word >> LB) << LB | (REFINE(tile,p,a).x & (2^LB-1)).
+ *  NARROW one STEP draw per pair of same-colour tiles (tx, tx+2) of a row (c0 = ty*ceil(Tx/4) + tx/4);
+ *         tile half h = (tx>>1)&1 uses words 2h, 2h+1; attempt a uses 16-bit half (a&1) of word
+ *         2h+(a>>1): bits [0,LB) direction/cell, action x = (half >> LB) << (32-(16-LB))
+ *         | (REFINE(tile,p,a).x & (2^(16+LB)-1)).
+ * In both formats the action word is a uniform 32-bit value assembled from disjoint Philox bits, so
+ * the rule sees exactly the reference's action distribution. */
+static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a, uint32_t* low, uint32_t* hi_part,
+                             int* hi_shift) {
+    if (!narrow) {
+        *low = w[a] & ((1u << lb) - 1u);
+        *hi_part = w[a] >> lb;
+        *hi_shift = lb;
+    } else {
+        const uint32_t half = (w[2 * h + (a >> 1)] >> (16 * (a & 1))) & 0xFFFFu;
+        *low = half & ((1u << lb) - 1u);
+        *hi_part = half >> lb;
+        *hi_shift = 32 - (16 - lb);
     }
 }
 
@@ -446,7 +480,7 @@ EXPORT void orc_crs_init(int length, int height, int species, double empty_prob,
  * colour have disjoint footprints, so the order within a phase is immaterial; this loop is the
  * sequential definition the GPU kernels must reproduce bit-for-bit.  Returns 0 / 5 / 2. */
 EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int arity, int flux,
-                       const double* dom, double mobility, uint64_t seed, int64_t mcs0, int64_t n_mcs) {
+                       const double* dom, double mobility, uint64_t seed, int64_t mcs0, int64_t n_mcs, int narrow) {
     orc_ctx c;
     const int periodic = flux != 0;
     const int db = arity == 8 ? 3 : 2;
@@ -457,21 +491,24 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
         int oy, ox, perm[4];
         orc_crs_round(seed, (uint64_t)mcs, &oy, &ox, perm);
         const int ty_n = crs_tiles(height, oy, periodic), tx_n = crs_tiles(length, ox, periodic);
+        const int tq = (tx_n + 3) / 4;
         for (int p = 0; p < 4; ++p) {
             const int cy = perm[p] >> 1, cx = perm[p] & 1;
             for (int ty = cy; ty < ty_n; ty += 2) {
                 for (int tx = cx; tx < tx_n; tx += 2) {
                     const uint32_t tile = (uint32_t)ty * (uint32_t)tx_n + (uint32_t)tx;
+                    const uint32_t sid = narrow ? (uint32_t)ty * (uint32_t)tq + (uint32_t)(tx >> 2) : tile;
+                    const int h = (tx >> 1) & 1;
                     uint32_t w[4];
-                    crs_draw(seed, tile, (uint64_t)mcs, ((uint32_t)DOM_STEP << 8) | (uint32_t)p, w);
+                    crs_draw(seed, sid, (uint64_t)mcs, DOM_STEP, (uint32_t)p, 0, w);
                     for (int a = 0; a < 4; ++a) {
-                        uint32_t rf[4];
-                        const uint32_t word = w[a];
-                        const int dir = (int)(word & (uint32_t)(arity - 1));
-                        const int dy = (int)((word >> db) & 1u), dx = (int)((word >> (db + 1)) & 1u);
-                        crs_draw(seed, tile, (uint64_t)mcs,
-                                 ((uint32_t)DOM_REFINE << 8) | ((uint32_t)p << 2) | (uint32_t)a, rf);
-                        const uint32_t x = ((word >> lb) << lb) | (rf[0] & ((1u << lb) - 1u));
+                        uint32_t rf[4], low, hi_part;
+                        int hi_shift;
+                        crs_attempt_bits(narrow, lb, w, h, a, &low, &hi_part, &hi_shift);
+                        const int dir = (int)(low & (uint32_t)(arity - 1));
+                        const int dy = (int)((low >> db) & 1u), dx = (int)((low >> (db + 1)) & 1u);
+                        crs_draw(seed, tile, (uint64_t)mcs, DOM_REFINE, (uint32_t)p, (uint32_t)a, rf);
+                        const uint32_t x = (hi_part << hi_shift) | (rf[0] & ((1u << hi_shift) - 1u));
                         int y = 2 * ty - oy + dy, xc = 2 * tx - ox + dx;
                         if (periodic) {
                             y = (y + height) % height;

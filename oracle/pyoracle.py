@@ -88,7 +88,9 @@ class Oracle:
         L.orc_crs_init.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, _i32]
         L.orc_crs_run.restype = C.c_int
         L.orc_crs_run.argtypes = [_i32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f64, C.c_double, C.c_uint64,
-                                  C.c_int64, C.c_int64]
+                                  C.c_int64, C.c_int64, C.c_int]
+        L.orc_seed32.restype = C.c_uint32
+        L.orc_seed32.argtypes = [C.c_uint64]
 
     # --- RNG -----------------------------------------------------------------------------
     def mt_words(self, seed32, n):
@@ -169,11 +171,12 @@ class Oracle:
         self.lib.orc_crs_init(length, height, species, empty_prob, seed, cells)
         return cells
 
-    def crs_run(self, cells, length, height, dom, mobility, seed, mcs0, n_mcs, arity=4, flux=True):
+    def crs_run(self, cells, length, height, dom, mobility, seed, mcs0, n_mcs, arity=4, flux=True, narrow=False):
         species = int(round(np.sqrt(np.asarray(dom).size)))
         cells = np.ascontiguousarray(cells, np.int32).copy()
         rc = self.lib.orc_crs_run(cells, length, height, species, arity, int(flux),
-                                  np.ascontiguousarray(dom, np.float64).ravel(), mobility, seed, mcs0, n_mcs)
+                                  np.ascontiguousarray(dom, np.float64).ravel(), mobility, seed, mcs0, n_mcs,
+                                  int(bool(narrow)))
         if rc:
             raise RuntimeError("oracle crs error %d" % rc)
         return cells

@@ -2,24 +2,27 @@
 //
 // One MCS = one round of four colour phases.  Per round a Philox draw picks the 2x2 tiling origin
 // (oy, ox) and the colour order; in each phase every tile of that colour performs 4 sequential
-// elementary steps (engine.hpp:108-141) with cell, direction and action drawn from one Philox
-// call keyed by (seed) and countered by (tile, mcs, phase).  Same-colour tiles have disjoint
-// footprints, so each phase is an exact random-sequential update of its tiles in any order.
-// oracle/escg_oracle.c:orc_crs_run is the sequential definition these kernels reproduce bit-exactly.
+// elementary steps (engine.hpp:108-141) with cell, direction and action drawn from counter-based
+// Philox words.  Same-colour tiles have disjoint footprints, so a phase is an exact
+// random-sequential update of its tiles in any order.  oracle/escg_oracle.c:orc_crs_run is the
+// sequential definition these kernels reproduce bit-exactly (draw spec: DESIGN.md §RNG).
 #pragma once
 #include <cstdint>
 
 namespace escgd {
 
 constexpr uint32_t kDomStep = 0, kDomRefine = 1, kDomRound = 2, kDomInit = 3;
+constexpr uint32_t kKey0 = 0xA4093822u, kKey1 = 0x299F31D0u;
 
-// Philox4x32-10 (Salmon et al. SC'11).  mul.wide.u32 → one IMAD.WIDE.U32 per product.
-__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
-                                        uint32_t k1) {
+// Philox4x32-10 (Salmon et al. SC'11) with the fixed key: every round key is an immediate, so a
+// round is 2 IMAD.WIDE.U32 + 2 LOP3.
+__device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+    uint32_t k0 = kKey0, k1 = kKey1;
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
-        const uint64_t p0 = static_cast<uint64_t>(c0) * 0xD2511F53u;
-        const uint64_t p1 = static_cast<uint64_t>(c2) * 0xCD9E8D57u;
+        uint64_t p0, p1;
+        asm("mul.wide.u32 %0, %1, %2;" : "=l"(p0) : "r"(c0), "r"(0xD2511F53u));
+        asm("mul.wide.u32 %0, %1, %2;" : "=l"(p1) : "r"(c2), "r"(0xCD9E8D57u));
         const uint32_t n0 = static_cast<uint32_t>(p1 >> 32) ^ c1 ^ k0;
         const uint32_t n2 = static_cast<uint32_t>(p0 >> 32) ^ c3 ^ k1;
         c1 = static_cast<uint32_t>(p1);
@@ -32,19 +35,24 @@ __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, u
     return make_uint4(c0, c1, c2, c3);
 }
 
-// Counter word 2: mcs bits 32..47 | domain | low field.
-__device__ __forceinline__ uint32_t ctr2(uint64_t mcs, uint32_t dom, uint32_t low) {
-    return (static_cast<uint32_t>((mcs >> 32) & 0xFFFFu) << 16) | (dom << 8) | low;
+__host__ __device__ __forceinline__ uint32_t murmur_finalize(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x85ebca6bu;
+    x ^= x >> 13;
+    x *= 0xc2b2ae35u;
+    x ^= x >> 16;
+    return x;
 }
 
-// Integer form of the reference's action bucketing (engine.hpp:117-123): migration iff x < xm,
-// interaction iff xm <= x < xi, reproduction iff x >= xi.  Coarse copies (x >> LB) let the hot
-// loop decide with the 28/27 high bits of the step word; a word whose coarse part equals a
-// threshold's coarse part draws its low LB bits from the REFINE domain (exact, rare).
-struct Rule {
-    uint32_t xm, xi;      // full thresholds
-    uint32_t xm_c, xi_c;  // coarse thresholds
-};
+// c3 of every draw: the seed folded to 32 bits (identity for seeds < 2^32).
+__host__ __device__ __forceinline__ uint32_t seed32(uint64_t seed) {
+    return static_cast<uint32_t>(seed) ^ murmur_finalize(static_cast<uint32_t>(seed >> 32));
+}
+
+// c2 of every draw: mcs bits 32..47 | domain << 16 | phase << 20 | attempt << 24.
+__host__ __device__ __forceinline__ uint32_t ctr2(uint64_t mcs, uint32_t dom, uint32_t phase, uint32_t attempt) {
+    return (static_cast<uint32_t>(mcs >> 32) & 0xFFFFu) | (dom << 16) | (phase << 20) | (attempt << 24);
+}
 
 // Round parameters (orc_crs_round): origin (oy, ox) and the four colours in phase order.
 struct Round {
@@ -53,11 +61,11 @@ struct Round {
     __device__ __forceinline__ int colour(int p) const { return static_cast<int>((order >> (2 * p)) & 3u); }
 };
 
-__device__ __forceinline__ Round round_params(uint32_t k0, uint32_t k1, uint64_t mcs) {
+__device__ __forceinline__ Round round_params(uint32_t s32, uint64_t mcs) {
     // Lexicographic permutations of {0,1,2,3}, packed 2 bits per colour (phase 0 in bits 0-1).
     constexpr uint8_t kPerm[24] = {0xE4, 0xB4, 0xD8, 0x78, 0x9C, 0x6C, 0xE1, 0xB1, 0xC9, 0x39, 0x8D, 0x2D,
                                    0xD2, 0x72, 0xC6, 0x36, 0x4E, 0x1E, 0x93, 0x63, 0x87, 0x27, 0x4B, 0x1B};
-    const uint4 w = philox(0u, static_cast<uint32_t>(mcs), ctr2(mcs, kDomRound, 0u), 0u, k0, k1);
+    const uint4 w = philox(0u, static_cast<uint32_t>(mcs), ctr2(mcs, kDomRound, 0u, 0u), s32);
     Round r;
     r.oy = static_cast<int>(w.x & 1u);
     r.ox = static_cast<int>((w.x >> 1) & 1u);
@@ -67,131 +75,238 @@ __device__ __forceinline__ Round round_params(uint32_t k0, uint32_t k1, uint64_t
 }
 
 // (drow, dcol) of direction d (params.hpp:81: up, down, left, right, ul, ur, dl, dr).
-template <int ARITY>
-__device__ __forceinline__ void dir_rc(uint32_t d, int& dr, int& dc) {
+__host__ __device__ __forceinline__ void dir_rc(uint32_t d, int& dr, int& dc) {
     dr = (d < 4u) ? ((d < 2u) ? ((d & 1u) ? 1 : -1) : 0) : ((d & 2u) ? 1 : -1);
     dc = (d < 4u) ? ((d < 2u) ? 0 : ((d & 1u) ? 1 : -1)) : ((d & 1u) ? 1 : -1);
-}
-
-// Neighbour offset in a row-major window of pitch P.
-template <int ARITY>
-__device__ __forceinline__ int dir_offset(uint32_t d, int P) {
-    if (ARITY == 4) {
-        const int m = (d & 2u) ? 1 : P;
-        return (d & 1u) ? m : -m;
-    } else {
-        int dr, dc;
-        dir_rc<ARITY>(d, dr, dc);
-        return dr * P + dc;
-    }
 }
 
 template <int ARITY>
 struct Bits {
     static constexpr int DB = ARITY == 8 ? 3 : 2;  // direction bits
-    static constexpr int LB = DB + 2;              // low bits (direction + cell) = refine width
+    static constexpr int LB = DB + 2;              // direction + cell bits of an attempt
+    static constexpr int NT = 1 << LB;             // offset-table entries
+    static constexpr int CBN = 16 - LB;            // coarse action bits of a NARROW attempt
 };
 
-// Low LB bits of attempt `a` of a tile, from the REFINE domain.
-template <int ARITY>
-__device__ __noinline__ uint32_t refine_bits(uint32_t k0, uint32_t k1, uint32_t tile, uint64_t mcs, int phase,
-                                             int a) {
-    const uint4 r = philox(tile, static_cast<uint32_t>(mcs),
-                           ctr2(mcs, kDomRefine, (static_cast<uint32_t>(phase) << 2) | static_cast<uint32_t>(a)), 0u,
-                           k0, k1);
-    return r.x & ((1u << Bits<ARITY>::LB) - 1u);
+// ---- 32-bit shared-memory access (volatile: keeps the sequential attempts in program order) ----
+__device__ __forceinline__ uint32_t lds8(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts8(uint32_t a, uint32_t v) { asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ uint2 lds64(uint32_t a) {
+    uint2 v;
+    asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// The rule on one (cell, neighbour) pair with action word x (engine.hpp:111-140).  sT is the
-// (S+1)^2 interaction-threshold table: u < D[a][b] (engine.hpp:125-131) ⇔ x < sT[a*S1+b].
-// `x` holds the coarse word; `refine()` supplies the exact low bits when a comparison needs them.
-template <int ARITY, class Refine>
-__device__ __forceinline__ void apply_rule(uint32_t s, uint32_t n, uint32_t word, const Rule& R,
-                                           const uint32_t* __restrict__ sT, int S1, uint32_t& ns, uint32_t& nn,
-                                           Refine refine) {
-    constexpr int LB = Bits<ARITY>::LB;
-    const uint32_t coarse = word >> LB;
-    uint32_t x = coarse << LB;
-    bool exact = false;
-    if ((coarse == R.xm_c) | (coarse == R.xi_c)) {
-        x |= refine();
-        exact = true;
+// Offset table: entry (dir | dy << DB | dx << DB+1) = (cell offset, neighbour offset) from the
+// tile's (0,0) cell in a row-major window of pitch P.
+template <int ARITY>
+__device__ __forceinline__ void build_offset_table(int2* tbl, int P) {
+    for (int e = threadIdx.x; e < Bits<ARITY>::NT; e += blockDim.x) {
+        const uint32_t d = static_cast<uint32_t>(e) & (ARITY - 1);
+        const int dy = (e >> Bits<ARITY>::DB) & 1, dx = (e >> (Bits<ARITY>::DB + 1)) & 1;
+        int dr, dc;
+        dir_rc(d, dr, dc);
+        const int so = dy * P + dx;
+        tbl[e] = make_int2(so, so + dr * P + dc);
     }
-    ns = s;
-    nn = n;
-    if (x < R.xm) {  // migration: exchange (engine.hpp:118-122)
+}
+
+// Per-CTA, per-phase constants of the attempt loop (kept in registers; slow paths get them by value).
+struct PhaseCtx {
+    uint32_t tbl;            // smem address of the offset table
+    uint32_t fast;           // attempt bits below this are certain migrations (NARROW fast path)
+    uint32_t xm, xi;         // X_mig, X_int
+    uint32_t sT;             // smem address of the (S+1)^2 interaction thresholds
+    int S1;
+    uint32_t c1, c2ref, c3;  // draw counter words (c2ref: REFINE domain, phase set, attempt 0)
+};
+
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// REFINE-domain word of attempt a of `tile` (exact action completion; rare).
+__device__ __noinline__ uint32_t refine_word(uint32_t tile, int a, uint32_t c1, uint32_t c2ref, uint32_t c3) {
+    return philox(tile, c1, c2ref | (static_cast<uint32_t>(a) << 24), c3).x;
+}
+
+// The rule (engine.hpp:111-140) on (s, n) with the exact 32-bit action word x:
+// migration iff x < X_mig, interaction iff X_mig <= x < X_int, else reproduction; interaction
+// outcome u < D[a][b] (engine.hpp:125-131) ⇔ x < T[a][b].  Returns ns | nn << 8.
+__device__ __forceinline__ uint32_t rule_exact(uint32_t s, uint32_t n, uint32_t x, uint32_t xm, uint32_t xi,
+                                               const uint32_t* T, int S1) {
+    uint32_t ns = s, nn = n;
+    if (x < xm) {
         ns = n;
         nn = s;
-    } else if (x >= R.xi) {  // reproduction into an empty site (engine.hpp:134-140)
+    } else if (x >= xi) {
         if (n == 0u)
             nn = s;
         else if (s == 0u)
             ns = n;
-    } else if ((s != 0u) & (n != 0u) & (s != n)) {  // interaction (engine.hpp:123-133)
-        const uint32_t t1 = sT[s * S1 + n], t2 = sT[n * S1 + s];
-        if (!exact && ((coarse == (t1 >> LB)) | (coarse == (t2 >> LB)))) x |= refine();
-        if (x < t1)
+    } else if ((s != 0u) & (n != 0u) & (s != n)) {
+        if (x < T[s * S1 + n])
             nn = 0u;
-        else if (x < t2)
+        else if (x < T[n * S1 + s])
             ns = 0u;
     }
+    return ns | (nn << 8);
 }
 
-// Four sequential attempts of one tile whose (0,0) cell sits at window offset `base`
-// (periodic / contiguous-window addressing: every footprint cell is at base + small offset).
+// Same rule reading the thresholds from shared memory (32-bit address).
+__device__ __forceinline__ uint32_t rule_exact_s(uint32_t s, uint32_t n, uint32_t x, uint32_t xm, uint32_t xi,
+                                                 uint32_t sT, int S1) {
+    uint32_t ns = s, nn = n;
+    if (x < xm) {
+        ns = n;
+        nn = s;
+    } else if (x >= xi) {
+        if (n == 0u)
+            nn = s;
+        else if (s == 0u)
+            ns = n;
+    } else if ((s != 0u) & (n != 0u) & (s != n)) {
+        if (x < lds32(sT + 4u * (s * S1 + n)))
+            nn = 0u;
+        else if (x < lds32(sT + 4u * (n * S1 + s)))
+            ns = 0u;
+    }
+    return ns | (nn << 8);
+}
+
+// WIDE exact path: the low LB bits come from REFINE (taken only when a consulted threshold
+// shares the coarse value of the word).
 template <int ARITY>
-__device__ __forceinline__ void tile_attempts(uint8_t* __restrict__ lat, int base, int P, const uint4 w,
-                                              const Rule& R, const uint32_t* __restrict__ sT, int S1, uint32_t k0,
-                                              uint32_t k1, uint32_t tile, uint64_t mcs, int phase) {
-    constexpr int DB = Bits<ARITY>::DB;
-    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const uint32_t word = words[a];
-        const uint32_t d = word & (ARITY - 1);
-        const int sa = base + static_cast<int>((word >> DB) & 1u) * P + static_cast<int>((word >> (DB + 1)) & 1u);
-        const int na = sa + dir_offset<ARITY>(d, P);
-        const uint32_t s = lat[sa], n = lat[na];
-        uint32_t ns, nn;
-        apply_rule<ARITY>(s, n, word, R, sT, S1, ns, nn,
-                          [&]() { return refine_bits<ARITY>(k0, k1, tile, mcs, phase, a); });
-        lat[sa] = static_cast<uint8_t>(ns);
-        lat[na] = static_cast<uint8_t>(nn);
+__device__ __noinline__ uint32_t slow_wide(uint32_t s, uint32_t n, uint32_t word, uint32_t tile, int a, uint32_t xm,
+                                           uint32_t xi, uint32_t sT, int S1, uint32_t c1, uint32_t c2ref,
+                                           uint32_t c3) {
+    constexpr int LB = Bits<ARITY>::LB;
+    const uint32_t x = ((word >> LB) << LB) | (refine_word(tile, a, c1, c2ref, c3) & ((1u << LB) - 1u));
+    return rule_exact_s(s, n, x, xm, xi, sT, S1);
+}
+
+// NARROW slow path: x = coarse(16-LB bits) << (16+LB) | low (16+LB) bits of the REFINE word.
+template <int ARITY>
+__device__ __noinline__ uint32_t slow_narrow(uint32_t s, uint32_t n, uint32_t half, uint32_t tile, int a,
+                                             uint32_t xm, uint32_t xi, uint32_t sT, int S1, uint32_t c1,
+                                             uint32_t c2ref, uint32_t c3) {
+    constexpr int LB = Bits<ARITY>::LB, SH = 16 + LB;
+    const uint32_t x = ((half >> LB) << SH) | (refine_word(tile, a, c1, c2ref, c3) & ((1u << SH) - 1u));
+    return rule_exact_s(s, n, x, xm, xi, sT, S1);
+}
+
+// WIDE rule on the coarse word (low LB bits zero).  A comparison against threshold T is decided by
+// the coarse bits unless coarse == T >> LB; those (rare) words take the exact path.
+template <int ARITY>
+__device__ __forceinline__ uint32_t rule_wide(uint32_t s, uint32_t n, uint32_t word, uint32_t tile, int a,
+                                              const PhaseCtx& C) {
+    constexpr uint32_t HI = ~((1u << Bits<ARITY>::LB) - 1u);
+    const uint32_t x = word & HI;
+    bool exact = (x == (C.xm & HI)) | (x == (C.xi & HI));
+    uint32_t ns = s, nn = n;
+    if (!exact) {
+        if (x < C.xm) {
+            ns = n;
+            nn = s;
+        } else if (x >= C.xi) {
+            if (n == 0u)
+                nn = s;
+            else if (s == 0u)
+                ns = n;
+        } else if ((s != 0u) & (n != 0u) & (s != n)) {
+            const uint32_t t1 = lds32(C.sT + 4u * (s * C.S1 + n)), t2 = lds32(C.sT + 4u * (n * C.S1 + s));
+            exact = (x == (t1 & HI)) | (x == (t2 & HI));
+            if (x < t1)
+                nn = 0u;
+            else if (x < t2)
+                ns = 0u;
+        }
+    }
+    if (exact) return slow_wide<ARITY>(s, n, word, tile, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+    return ns | (nn << 8);
+}
+
+// One attempt: `bits` is the 32-bit word (WIDE) or the zero-extended 16-bit half (NARROW).
+template <int ARITY, bool NARROW>
+__device__ __forceinline__ void attempt(uint32_t bits, uint32_t base, uint32_t tile, int a, const PhaseCtx& C) {
+    const uint2 t = lds64(C.tbl + ((bits & (Bits<ARITY>::NT - 1)) << 3));
+    const uint32_t sa = base + t.x, na = base + t.y;
+    const uint32_t s = lds8(sa), n = lds8(na);
+    if (NARROW) {
+        if (bits < C.fast) {  // certain migration: exchange (engine.hpp:118-122); s == n is a no-op
+            if (s != n) {
+                sts8(sa, n);
+                sts8(na, s);
+            }
+            return;
+        }
+        const uint32_t r = slow_narrow<ARITY>(s, n, bits, tile, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+        sts8(sa, r & 0xFFu);
+        sts8(na, r >> 8);
+    } else {
+        const uint32_t r = rule_wide<ARITY>(s, n, bits, tile, a, C);
+        if (s != n) {  // engine.hpp:113: equal pairs never change
+            sts8(sa, r & 0xFFu);
+            sts8(na, r >> 8);
+        }
     }
 }
 
-// Mirror-reflect variant (flux=false, lattice.hpp:42-47): tile cells outside the lattice are
-// skipped (partial edge tiles), neighbours reflect one step inward.  (y0, x0) are the global
-// coordinates of the tile's (0,0) cell; the window maps global (y, x) to (y+R0)*P + x + C0.
+// Four attempts of a WIDE tile from its own STEP draw.
 template <int ARITY>
-__device__ __forceinline__ void tile_attempts_reflect(uint8_t* __restrict__ lat, int y0, int x0, int R0, int C0,
-                                                      int P, int H, int L, const uint4 w, const Rule& R,
-                                                      const uint32_t* __restrict__ sT, int S1, uint32_t k0,
-                                                      uint32_t k1, uint32_t tile, uint64_t mcs, int phase) {
+__device__ __forceinline__ void tile_wide(const uint4 w, uint32_t base, uint32_t tile, const PhaseCtx& C) {
+    attempt<ARITY, false>(w.x, base, tile, 0, C);
+    attempt<ARITY, false>(w.y, base, tile, 1, C);
+    attempt<ARITY, false>(w.z, base, tile, 2, C);
+    attempt<ARITY, false>(w.w, base, tile, 3, C);
+}
+
+// Four attempts of half h of a NARROW pair draw (words 2h, 2h+1; low half first).
+template <int ARITY>
+__device__ __forceinline__ void tile_narrow(uint32_t wa, uint32_t wb, uint32_t base, uint32_t tile,
+                                            const PhaseCtx& C) {
+    attempt<ARITY, true>(wa & 0xFFFFu, base, tile, 0, C);
+    attempt<ARITY, true>(wa >> 16, base, tile, 1, C);
+    attempt<ARITY, true>(wb & 0xFFFFu, base, tile, 2, C);
+    attempt<ARITY, true>(wb >> 16, base, tile, 3, C);
+}
+
+// Mirror-reflect variant (flux=false, lattice.hpp:42-47; WIDE format only): tile cells outside the
+// lattice are skipped (partial edge tiles), neighbours reflect one step inward.  (y0, x0) are the
+// global coordinates of the tile's (0,0) cell; the window maps (y, x) to lat0 + (y+R0)*P + x + C0.
+template <int ARITY>
+__device__ __forceinline__ void tile_reflect(const uint4 w, uint32_t lat0, int y0, int x0, int R0, int C0, int P,
+                                             int H, int L, uint32_t tile, const PhaseCtx& C) {
     constexpr int DB = Bits<ARITY>::DB;
     const uint32_t words[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const uint32_t word = words[a];
-        const uint32_t d = word & (ARITY - 1);
         const int y = y0 + static_cast<int>((word >> DB) & 1u);
         const int x = x0 + static_cast<int>((word >> (DB + 1)) & 1u);
         if (y < 0 || y >= H || x < 0 || x >= L) continue;
         int dr, dc;
-        dir_rc<ARITY>(d, dr, dc);
+        dir_rc(word & (ARITY - 1), dr, dc);
         int ny = y + dr, nx = x + dc;
         if (ny < 0) ny = -ny;
         if (ny >= H) ny = 2 * (H - 1) - ny;
         if (nx < 0) nx = -nx;
         if (nx >= L) nx = 2 * (L - 1) - nx;
-        const int sa = (y + R0) * P + x + C0;
-        const int na = (ny + R0) * P + nx + C0;
-        const uint32_t s = lat[sa], n = lat[na];
-        uint32_t ns, nn;
-        apply_rule<ARITY>(s, n, word, R, sT, S1, ns, nn,
-                          [&]() { return refine_bits<ARITY>(k0, k1, tile, mcs, phase, a); });
-        lat[sa] = static_cast<uint8_t>(ns);
-        lat[na] = static_cast<uint8_t>(nn);
+        const uint32_t sa = lat0 + static_cast<uint32_t>((y + R0) * P + x + C0);
+        const uint32_t na = lat0 + static_cast<uint32_t>((ny + R0) * P + nx + C0);
+        const uint32_t s = lds8(sa), n = lds8(na);
+        const uint32_t r = rule_wide<ARITY>(s, n, word, tile, a, C);
+        sts8(sa, r & 0xFFu);
+        sts8(na, r >> 8);
     }
 }
 

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -180,6 +181,7 @@ struct escg_dev {
     int smem = 0;
     int P = 0;
     int nby = 1, nbx = 1;
+    int narrow = 0;  // draw format
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     Thresholds th;
@@ -211,21 +213,27 @@ struct escg_dev {
 
 namespace {
 
-// Block-kernel decomposition: row/col splits at multiples of 4 minimising waves x window area.
+// Block-kernel decomposition: row splits at multiples of 4, column splits at multiples of 8 when
+// L % 8 == 0 (keeps NARROW tile pairs aligned), minimising waves x computed window area.
+size_t block_smem(int bh, int bw, int S1, int* pitch) {
+    const int P = ((bw + 2 * escgd::kMarginX) + 15) & ~15;
+    if (pitch) *pitch = P;
+    return static_cast<size_t>((((bh + 2 * escgd::kMargin) * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8 +
+                               (escgd::kMaxSpecies + 1) * 4 + 64);
+}
+
 void plan_blocks(escg_dev* h, int sms, int smem_cap) {
-    const int uy = h->H / 4, ux = h->L / 4;
+    const int cu = (h->L % 16 == 0) ? 16 : ((h->L % 8 == 0) ? 8 : 4);
+    const int uy = h->H / 4, ux = h->L / cu;
     double best = 1e300;
     int bnby = 1, bnbx = 1;
-    const int M = escgd::kMargin;
     for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
         for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
-            const int bh = ((uy + nby - 1) / nby) * 4, bw = ((ux + nbx - 1) / nbx) * 4;
-            const int Pw = ((bw + 2 * M) + 15) & ~15;
-            const int bytes = (bh + 2 * M) * Pw + h->S1 * h->S1 * 4 + (escgd::kMaxSpecies + 1) * 4 + 64;
-            if (bytes > smem_cap) continue;
+            const int bh = ((uy + nby - 1) / nby) * 4, bw = ((ux + nbx - 1) / nbx) * cu;
+            if (block_smem(bh, bw, h->S1, nullptr) > static_cast<size_t>(smem_cap)) continue;
             const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
             const int64_t waves = (ctas + sms - 1) / sms;
-            // compute ∝ average valid area over the 4 phases (margin 12 → mean extra ~6 per side)
+            // compute ∝ average valid area over the 4 phases (12-cell margin → ~6 extra per side)
             const double cost = static_cast<double>(waves) * (bh + 12.0) * (bw + 12.0) + 2000.0 * waves;
             if (cost < best) {
                 best = cost;
@@ -238,12 +246,11 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap) {
     h->nbx = bnbx;
     std::vector<int> rows(bnby + 1), cols(bnbx + 1);
     for (int i = 0; i <= bnby; ++i) rows[i] = static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
-    for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(ux) * i / bnbx) * 4;
+    for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(ux) * i / bnbx) * cu;
     int bh = 0, bw = 0;
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
-    h->P = ((bw + 2 * M) + 15) & ~15;
-    h->smem = (((bh + 2 * M) * h->P + 15) & ~15) + h->S1 * h->S1 * 4 + (escgd::kMaxSpecies + 1) * 4 + 64;
+    h->smem = static_cast<int>(block_smem(bh, bw, h->S1, &h->P));
     h->d_rows.alloc(rows.size());
     h->d_cols.alloc(cols.size());
     CK(cudaMemcpy(h->d_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
@@ -316,6 +323,7 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.S = h->S;
     a.P = h->P;
     a.arity = h->arity;
+    a.narrow = h->narrow;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -376,6 +384,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.P = h->P;
         a.arity = h->arity;
         a.flux = h->flux;
+        a.narrow = h->narrow;
         a.record = 1;
         a.smem_bytes = h->smem;
         CK(escgd::launch_tile(a, h->nrep, h->threads, h->stream));
@@ -396,6 +405,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.S = h->S;
         a.P = h->P;
         a.arity = h->arity;
+        a.narrow = h->narrow;
         a.nby = h->nby;
         a.nbx = h->nbx;
         a.row_split = h->d_rows.p;
@@ -563,6 +573,17 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
         if (choice == ESCG_KERNEL_BLOCK && !periodic4)
             config_error("block kernel supports periodic (flux) lattices only");
         h->kernel = choice;
+        // NARROW (16-bit attempt words, one draw per tile pair) when migrations dominate so much that
+        // at most 1/64 of attempts leave the coarse fast path; needs periodic wrap and L % 8 == 0.
+        {
+            const int LB = h->arity == 8 ? 5 : 4, CB = 16 - LB;
+            const uint64_t fast_coarse = h->th.xm >> (32 - CB);
+            h->narrow = (h->flux && h->L % 8 == 0 && fast_coarse * 64 >= 63ull * (1ull << CB)) ? 1 : 0;
+            if (const char* f = std::getenv("ESCG_DRAW_FORMAT")) {
+                if (std::strcmp(f, "wide") == 0) h->narrow = 0;
+                if (std::strcmp(f, "narrow") == 0 && h->flux && h->L % 8 == 0) h->narrow = 1;
+            }
+        }
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&h->ev0));
         CK(cudaEventCreate(&h->ev1));
@@ -688,6 +709,7 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
             a.P = h->P;
             a.arity = h->arity;
             a.flux = h->flux;
+            a.narrow = h->narrow;
             a.record = 0;
             a.smem_bytes = h->smem;
             // per-replica limit: all replicas advance by n_mcs from their own MCS; the kernel
@@ -809,6 +831,13 @@ int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t*
         if (grid_ctas) *grid_ctas = h->kernel == ESCG_KERNEL_TILE ? h->nrep : h->nby * h->nbx * h->nrep;
         if (threads) *threads = h->threads;
         if (smem_bytes) *smem_bytes = h->smem;
+    });
+}
+
+int escg_dev_draw_format(escg_dev* h, int32_t* narrow) {
+    return guarded([&] {
+        if (!h || !narrow) config_error("null argument");
+        *narrow = h->narrow;
     });
 }
 

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "crs.cuh"
 #include "launch.h"
@@ -50,36 +51,45 @@ __device__ int record_decide(const uint64_t* counts, int S1, int64_t mcs, int r,
     return st;
 }
 
-// Species histogram of a rows x cols region of a byte array with the given pitch into sCnt
-// (shared, zeroed by the caller).  S1 <= 8 uses SIMD byte compares + popc in registers.
+// n / d for 0 <= n < 2^22, 1 <= d < 2^22 via the float reciprocal (exact after one fix-up).
+__device__ __forceinline__ int udiv_small(int n, int d) {
+    int q = __float2int_rz(__int2float_rn(n) * __frcp_rn(__int2float_rn(d)));
+    int r = n - q * d;
+    if (r < 0) {
+        --q;
+    } else if (r >= d) {
+        ++q;
+    }
+    return q;
+}
+
+// Species histogram of a rows x cols region of a byte array (generic pointer, any space) with the
+// given pitch into sCnt (shared, zeroed by the caller).  Warps take rows, lanes take 4-byte words;
+// S1 <= 8 uses SIMD byte compares + popc in registers.
 __device__ void block_count(const uint8_t* base, int rows, int cols, int pitch, int S1, uint32_t* sCnt) {
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if (S1 <= 8 && (cols & 3) == 0 && (pitch & 3) == 0 && ((reinterpret_cast<uintptr_t>(base) & 3) == 0)) {
         uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const int wpr = cols >> 2;
-        const int total = rows * wpr;
-        for (int idx = tid; idx < total; idx += nt) {
-            const int y = idx / wpr;
-            const int x = idx - y * wpr;
-            const uint32_t w = *reinterpret_cast<const uint32_t*>(base + y * pitch + 4 * x);
+        for (int y = warp; y < rows; y += nw) {
+            const uint32_t* row = reinterpret_cast<const uint32_t*>(base + static_cast<size_t>(y) * pitch);
+            for (int x = lane; x < wpr; x += 32) {
+                const uint32_t w = row[x];
 #pragma unroll
-            for (int v = 0; v < 8; ++v)
-                if (v < S1) c[v] += __popc(__vcmpeq4(w, 0x01010101u * static_cast<uint32_t>(v)));
+                for (int v = 0; v < 8; ++v)
+                    if (v < S1) c[v] += __popc(__vcmpeq4(w, 0x01010101u * static_cast<uint32_t>(v)));
+            }
         }
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
             if (v < S1) {
                 const uint32_t s = __reduce_add_sync(0xffffffffu, c[v]);
-                if ((tid & 31) == 0 && s) atomicAdd(&sCnt[v], s >> 3);
+                if (lane == 0 && s) atomicAdd(&sCnt[v], s >> 3);
             }
         }
     } else {
-        const int total = rows * cols;
-        for (int idx = tid; idx < total; idx += nt) {
-            const int y = idx / cols;
-            const int x = idx - y * cols;
-            atomicAdd(&sCnt[base[y * pitch + x]], 1u);
-        }
+        for (int y = warp; y < rows; y += nw)
+            for (int x = lane; x < cols; x += 32) atomicAdd(&sCnt[base[static_cast<size_t>(y) * pitch + x]], 1u);
     }
 }
 
@@ -88,7 +98,7 @@ __device__ void block_count(const uint8_t* base, int rows, int cols, int pitch, 
 // ---------------------------------------------------------------------------------------------
 
 struct TileSmem {
-    int lat_bytes, T_off, snap_off, cnt_off, flag_off, total;
+    int lat_bytes, T_off, snap_off, cnt_off, flag_off, tbl_off, total;
 };
 
 __host__ __device__ inline TileSmem tile_layout(int H, int L, int S, int P) {
@@ -99,92 +109,144 @@ __host__ __device__ inline TileSmem tile_layout(int H, int L, int S, int P) {
     t.snap_off = t.T_off + align16(S1 * S1 * 4);
     t.cnt_off = t.snap_off + align16(3 * (L + 3) + 3 * H);
     t.flag_off = t.cnt_off + align16((kMaxSpecies + 1) * 4);
-    t.total = t.flag_off + 16;
+    t.tbl_off = t.flag_off + 16;
+    t.total = t.tbl_off + 32 * 8;
     return t;
-}
-
-// Ghost cell k → (gy, gx) in lattice coordinates (rows {-2,-1,H} x cols [-2,L], then
-// cols {-2,-1,L} x rows [0,H)).
-__device__ __forceinline__ void ghost_pos(int k, int H, int L, int& gy, int& gx) {
-    const int rowband = 3 * (L + 3);
-    if (k < rowband) {
-        const int b = k / (L + 3);
-        gx = k - b * (L + 3) - 2;
-        gy = b == 0 ? -2 : (b == 1 ? -1 : H);
-    } else {
-        const int k2 = k - rowband;
-        const int b = k2 / H;
-        gy = k2 - b * H;
-        gx = b == 0 ? -2 : (b == 1 ? -1 : L);
-    }
 }
 
 __device__ __forceinline__ int wrap(int v, int n) { return v < 0 ? v + n : (v >= n ? v - n : v); }
 
-// After a phase: a ghost that changed carries the phase's write of its physical cell (at most one
+// Ghost frame of the periodic tile kernel: rows {-2,-1,H} x cols [-2,L] and cols {-2,-1,L} x
+// rows [0,H).  Band b (0..5) enumerates them; snap holds the value each ghost had after refresh.
+// After a phase, a ghost that changed carries the phase's write of its physical cell (at most one
 // representation of a physical cell lies in an active footprint per phase).
-__device__ void ghost_fold(uint8_t* lat, const uint8_t* snap, int H, int L, int P) {
-    const int G = 3 * (L + 3) + 3 * H;
-    for (int k = threadIdx.x; k < G; k += blockDim.x) {
-        int gy, gx;
-        ghost_pos(k, H, L, gy, gx);
-        const uint8_t g = lat[(gy + kTileR0) * P + gx + kTileC0];
-        if (g != snap[k]) lat[(wrap(gy, H) + kTileR0) * P + wrap(gx, L) + kTileC0] = g;
+template <bool FOLD>
+__device__ void ghost_pass(uint8_t* lat, uint8_t* snap, int H, int L, int P) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int b = warp; b < 6; b += nw) {
+        const bool rowband = b < 3;
+        const int len = rowband ? L + 3 : H;
+        const int fixed = (b % 3) == 0 ? -2 : ((b % 3) == 1 ? -1 : (rowband ? H : L));
+        uint8_t* sn = snap + (rowband ? b * (L + 3) : 3 * (L + 3) + (b - 3) * H);
+        for (int k = lane; k < len; k += 32) {
+            const int gy = rowband ? fixed : k;
+            const int gx = rowband ? k - 2 : fixed;
+            const int ga = (gy + kTileR0) * P + gx + kTileC0;
+            const int pa = (wrap(gy, H) + kTileR0) * P + wrap(gx, L) + kTileC0;
+            if (FOLD) {
+                const uint8_t g = lat[ga];
+                if (g != sn[k]) lat[pa] = g;
+            } else {
+                const uint8_t v = lat[pa];
+                lat[ga] = v;
+                sn[k] = v;
+            }
+        }
     }
 }
 
-__device__ void ghost_refresh(uint8_t* lat, uint8_t* snap, int H, int L, int P) {
-    const int G = 3 * (L + 3) + 3 * H;
-    for (int k = threadIdx.x; k < G; k += blockDim.x) {
-        int gy, gx;
-        ghost_pos(k, H, L, gy, gx);
-        const uint8_t v = lat[(wrap(gy, H) + kTileR0) * P + wrap(gx, L) + kTileC0];
-        lat[(gy + kTileR0) * P + gx + kTileC0] = v;
-        snap[k] = v;
-    }
+template <int ARITY>
+__device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, uint32_t tbl, uint32_t sT, int S1,
+                                              uint64_t mcs, int p, uint32_t s32) {
+    constexpr int LB = Bits<ARITY>::LB;
+    PhaseCtx C;
+    C.tbl = tbl;
+    C.fast = narrow ? ((rule.xm >> (16 + LB)) << LB) : 0u;
+    C.xm = rule.xm;
+    C.xi = rule.xi;
+    C.sT = sT;
+    C.S1 = S1;
+    C.c1 = static_cast<uint32_t>(mcs);
+    C.c2ref = ctr2(mcs, kDomRefine, static_cast<uint32_t>(p), 0u);
+    C.c3 = s32;
+    return C;
 }
 
+// One MCS of the tile kernel (whole lattice in shared memory at lat0, ghost frame when periodic).
 template <int ARITY, bool REFLECT>
-__device__ void tile_round(uint8_t* lat, uint8_t* snap, const uint32_t* sT, const Rule& R, int H, int L, int P,
-                           int S1, uint32_t k0, uint32_t k1, uint64_t mcs) {
+__device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t tbl, uint32_t sT,
+                           const RuleArgs& rule, int narrow, int H, int L, int P, int S1, uint32_t s32,
+                           uint64_t mcs) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const Round rp = round_params(k0, k1, mcs);
+    const Round rp = round_params(s32, mcs);
     const int Ty = REFLECT ? (H + rp.oy + 1) >> 1 : H >> 1;
     const int Tx = REFLECT ? (L + rp.ox + 1) >> 1 : L >> 1;
 #pragma unroll 1
     for (int p = 0; p < 4; ++p) {
         const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-        const int nty = (Ty - cy + 1) >> 1, ntx = (Tx - cx + 1) >> 1;
-        const int cnt = nty * ntx;
+        const PhaseCtx C = phase_ctx<ARITY>(rule, narrow, tbl, sT, S1, mcs, p, s32);
+        const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+        const int nty = (Ty - cy + 1) >> 1;
+        // items: tiles (WIDE) or tile pairs (NARROW, periodic with L % 8 == 0) of this colour
+        const int nxi = (!REFLECT && narrow) ? (Tx >> 2) : ((Tx - cx + 1) >> 1);
+        const int cnt = nty * nxi;
         if (tid < cnt) {
-            int i = tid / ntx, j = tid - (tid / ntx) * ntx;
-            const int di = nt / ntx, dj = nt - (nt / ntx) * ntx;
-            const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p));
+            int i = udiv_small(tid, nxi), j = tid - udiv_small(tid, nxi) * nxi;
+            const int di = udiv_small(nt, nxi), dj = nt - udiv_small(nt, nxi) * nxi;
             for (int k = tid; k < cnt; k += nt) {
-                const int ty = cy + 2 * i, tx = cx + 2 * j;
-                const uint32_t tile = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(tx);
-                const uint4 w = philox(tile, static_cast<uint32_t>(mcs), c2, 0u, k0, k1);
-                if (REFLECT) {
-                    tile_attempts_reflect<ARITY>(lat, 2 * ty - rp.oy, 2 * tx - rp.ox, kTileR0, kTileC0, P, H, L, w, R,
-                                                 sT, S1, k0, k1, tile, mcs, p);
+                const int ty = cy + 2 * i;
+                if (!REFLECT && narrow) {
+                    const uint32_t pair = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx >> 2) + j;
+                    const uint4 w = philox(pair, C.c1, c2, s32);
+                    const int tx0 = cx + 4 * j;
+                    const uint32_t row = lat0 + static_cast<uint32_t>((2 * ty - rp.oy + kTileR0) * P + kTileC0 - rp.ox);
+                    const uint32_t t0 = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + tx0;
+                    tile_narrow<ARITY>(w.x, w.y, row + 2 * tx0, t0, C);
+                    tile_narrow<ARITY>(w.z, w.w, row + 2 * tx0 + 4, t0 + 2, C);
                 } else {
-                    const int base = (2 * ty - rp.oy + kTileR0) * P + (2 * tx - rp.ox + kTileC0);
-                    tile_attempts<ARITY>(lat, base, P, w, R, sT, S1, k0, k1, tile, mcs, p);
+                    const int tx = cx + 2 * j;
+                    const uint32_t tile = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(tx);
+                    const uint4 w = philox(tile, C.c1, c2, s32);
+                    if (REFLECT)
+                        tile_reflect<ARITY>(w, lat0, 2 * ty - rp.oy, 2 * tx - rp.ox, kTileR0, kTileC0, P, H, L, tile, C);
+                    else
+                        tile_wide<ARITY>(w, lat0 + static_cast<uint32_t>((2 * ty - rp.oy + kTileR0) * P + 2 * tx - rp.ox + kTileC0),
+                                         tile, C);
                 }
                 j += dj;
                 i += di;
-                if (j >= ntx) {
-                    j -= ntx;
+                if (j >= nxi) {
+                    j -= nxi;
                     ++i;
                 }
             }
         }
         __syncthreads();
         if (!REFLECT) {
-            ghost_fold(lat, snap, H, L, P);
+            ghost_pass<true>(lat, snap, H, L, P);
             __syncthreads();
-            ghost_refresh(lat, snap, H, L, P);
+            ghost_pass<false>(lat, snap, H, L, P);
             __syncthreads();
+        }
+    }
+}
+
+// Copy an H x L byte lattice between global (row pitch L) and shared (pitch P, origin R0/C0).
+template <bool TO_SMEM>
+__device__ void tile_copy(uint8_t* lat, uint8_t* glat, int H, int L, int P) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((L & 3) == 0) {
+        const int wpr = L >> 2;
+        for (int y = warp; y < H; y += nw) {
+            uint32_t* g = reinterpret_cast<uint32_t*>(glat + static_cast<size_t>(y) * L);
+            uint32_t* sm = reinterpret_cast<uint32_t*>(lat + (y + kTileR0) * P + kTileC0);
+            for (int c = lane; c < wpr; c += 32) {
+                if (TO_SMEM)
+                    sm[c] = g[c];
+                else
+                    g[c] = sm[c];
+            }
+        }
+    } else {
+        for (int y = warp; y < H; y += nw) {
+            uint8_t* g = glat + static_cast<size_t>(y) * L;
+            uint8_t* sm = lat + (y + kTileR0) * P + kTileC0;
+            for (int c = lane; c < L; c += 32) {
+                if (TO_SMEM)
+                    sm[c] = g[c];
+                else
+                    g[c] = sm[c];
+            }
         }
     }
 }
@@ -199,32 +261,21 @@ __global__ void __launch_bounds__(512) tile_kernel(TileArgs a) {
     uint8_t* snap = smem + lay.snap_off;
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + lay.cnt_off);
     int* sFlag = reinterpret_cast<int*>(smem + lay.flag_off);
+    int2* tblp = reinterpret_cast<int2*>(smem + lay.tbl_off);
     const int tid = threadIdx.x, nt = blockDim.x;
     const int r = blockIdx.x;
     uint8_t* glat = a.lat + static_cast<size_t>(r) * H * L;
-    const uint64_t seed = a.seeds[r];
-    const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
+    const uint32_t s32 = seed32(a.seeds[r]);
 
     for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
-    if ((L & 3) == 0) {
-        const int wpr = L >> 2;
-        for (int idx = tid; idx < H * wpr; idx += nt) {
-            const int y = idx / wpr, c = idx - (idx / wpr) * wpr;
-            *reinterpret_cast<uint32_t*>(lat + (y + kTileR0) * P + kTileC0 + 4 * c) =
-                *reinterpret_cast<const uint32_t*>(glat + static_cast<size_t>(y) * L + 4 * c);
-        }
-    } else {
-        for (int idx = tid; idx < H * L; idx += nt) {
-            const int y = idx / L, x = idx - (idx / L) * L;
-            lat[(y + kTileR0) * P + kTileC0 + x] = glat[idx];
-        }
-    }
+    build_offset_table<ARITY>(tblp, P);
+    tile_copy<true>(lat, glat, H, L, P);
     __syncthreads();
     if (!REFLECT) {
-        ghost_refresh(lat, snap, H, L, P);
+        ghost_pass<false>(lat, snap, H, L, P);
         __syncthreads();
     }
-    const Rule R{a.rule.xm, a.rule.xi, a.rule.xm >> Bits<ARITY>::LB, a.rule.xi >> Bits<ARITY>::LB};
+    const uint32_t lat0 = smem_addr(lat), tbl = smem_addr(tblp), sTa = smem_addr(sT);
     int64_t mcs = a.run.mcs[r];
     int status = a.run.status[r];
     for (;;) {
@@ -248,21 +299,10 @@ __global__ void __launch_bounds__(512) tile_kernel(TileArgs a) {
             adv = a.run.mcs_limit - mcs;
         }
         for (int64_t k = 0; k < adv; ++k, ++mcs)
-            tile_round<ARITY, REFLECT>(lat, snap, sT, R, H, L, P, S1, k0, k1, static_cast<uint64_t>(mcs));
+            tile_round<ARITY, REFLECT>(lat0, lat, snap, tbl, sTa, a.rule, a.narrow, H, L, P, S1, s32,
+                                       static_cast<uint64_t>(mcs));
     }
-    if ((L & 3) == 0) {
-        const int wpr = L >> 2;
-        for (int idx = tid; idx < H * wpr; idx += nt) {
-            const int y = idx / wpr, c = idx - (idx / wpr) * wpr;
-            *reinterpret_cast<uint32_t*>(glat + static_cast<size_t>(y) * L + 4 * c) =
-                *reinterpret_cast<const uint32_t*>(lat + (y + kTileR0) * P + kTileC0 + 4 * c);
-        }
-    } else {
-        for (int idx = tid; idx < H * L; idx += nt) {
-            const int y = idx / L, x = idx - (idx / L) * L;
-            glat[idx] = lat[(y + kTileR0) * P + kTileC0 + x];
-        }
-    }
+    tile_copy<false>(lat, glat, H, L, P);
     if (tid == 0 && !a.record) a.run.mcs[r] = mcs;
 }
 
@@ -270,94 +310,173 @@ __global__ void __launch_bounds__(512) tile_kernel(TileArgs a) {
 // Block kernel (overlapped tiling, one MCS per launch, periodic lattices with H, L ≡ 0 mod 4)
 // ---------------------------------------------------------------------------------------------
 
+// v mod n for v >= 0: one conditional subtract when the window is at most twice the lattice.
+__device__ __forceinline__ int wrap_down(int v, int n, bool big) {
+    if (big) return v % n;
+    return v >= n ? v - n : v;
+}
+
+template <int ARITY, bool NARROW>
+__device__ __forceinline__ void block_phases(const BlockArgs& a, uint32_t win0, uint32_t tbl, uint32_t sT, int S1,
+                                             int Wh, int Ww, int wy0, int wx0, uint32_t s32, uint64_t mcs) {
+    const int tid = threadIdx.x, nt = blockDim.x, P = a.P;
+    const Round rp = round_params(s32, mcs);
+    const int Ty = a.H >> 1, Tx = a.L >> 1, TQ = a.L >> 3;
+    const int jb = wy0 >> 1, ib = wx0 >> 1;  // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
+    const int ex = kMarginX - kMargin;        // extra loaded columns beyond the 12-cell margin
+    const bool big = Wh > a.H || Ww > a.L;    // window wraps more than once: use a true modulo
+#pragma unroll 1
+    for (int p = 0; p < 4; ++p) {
+        const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
+        const PhaseCtx C = phase_ctx<ARITY>(a.rule, NARROW, tbl, sT, S1, mcs, p, s32);
+        const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+        // footprint rows [2j-oy-1, 2j-oy+2] within [3p, Wh-3p); cols likewise within [ex+3p, Ww-ex-3p)
+        const int lo = 3 * p, hiR = Wh - 3 * p, loC = ex + 3 * p, hiC = Ww - ex - 3 * p;
+        const int jmin = (lo + rp.oy + 2) >> 1, jmax = (hiR - 3 + rp.oy) >> 1;
+        const int imin = (loC + rp.ox + 2) >> 1, imax = (hiC - 3 + rp.ox) >> 1;
+        const int j0 = jmin + ((jmin ^ cy) & 1);
+        const int nj = jmax >= j0 ? ((jmax - j0) >> 1) + 1 : 0;
+        int u0, nu;
+        if (NARROW) {
+            u0 = (imin - cx + 1) >> 2;
+            const int u1 = imax >= cx ? (imax - cx) >> 2 : -1;
+            nu = u1 >= u0 ? u1 - u0 + 1 : 0;
+        } else {
+            u0 = imin + ((imin ^ cx) & 1);
+            nu = imax >= u0 ? ((imax - u0) >> 1) + 1 : 0;
+        }
+        const int cnt = nj * nu;
+        if (tid < cnt) {
+            const int q0 = udiv_small(tid, nu), qn = udiv_small(nt, nu);
+            int aa = q0, bb = tid - q0 * nu;
+            const int da = qn, db = nt - qn * nu;
+            for (int k = tid; k < cnt; k += nt) {
+                const int j = j0 + 2 * aa;
+                const int ty = wrap_down(jb + j, Ty, big);
+                const uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
+                if (NARROW) {
+                    const int u = u0 + bb;
+                    const int q = wrap_down((ib >> 2) + u, TQ, big);
+                    const uint4 w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(TQ) + q, C.c1, c2, s32);
+                    const int i0 = cx + 4 * u;
+                    const uint32_t t0 = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + 4 * q + cx;
+                    if (i0 >= imin && i0 <= imax) tile_narrow<ARITY>(w.x, w.y, rowbase + 2 * i0, t0, C);
+                    if (i0 + 2 >= imin && i0 + 2 <= imax) tile_narrow<ARITY>(w.z, w.w, rowbase + 2 * i0 + 4, t0 + 2, C);
+                } else {
+                    const int i = u0 + 2 * bb;
+                    const int tx = wrap_down(ib + i, Tx, big);
+                    const uint32_t tile = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(tx);
+                    const uint4 w = philox(tile, C.c1, c2, s32);
+                    tile_wide<ARITY>(w, rowbase + 2 * i, tile, C);
+                }
+                bb += db;
+                aa += da;
+                if (bb >= nu) {
+                    bb -= nu;
+                    ++aa;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Window load (global → shared) with periodic wrap: warps take rows, lanes take VEC-byte chunks.
+template <int VEC>
+__device__ __forceinline__ void load_window(uint8_t* win, const uint8_t* src, int H, int L, int P, int Wh, int Ww,
+                                            int wy0, int wx0) {
+    using V = typename std::conditional<VEC == 16, uint4, uint32_t>::type;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int cpr = Ww / VEC;
+    const bool bigy = Wh > H, bigx = Ww > L;
+    for (int wr = warp; wr < Wh; wr += nw) {
+        int gy = wy0 + wr;
+        gy = bigy ? gy % H : (gy >= H ? gy - H : gy);
+        const uint8_t* srow = src + static_cast<size_t>(gy) * L;
+        V* drow = reinterpret_cast<V*>(win + wr * P);
+        for (int c = lane; c < cpr; c += 32) {
+            int gx = wx0 + VEC * c;
+            gx = bigx ? gx % L : (gx >= L ? gx - L : gx);
+            V v;
+            if (VEC == 16) {
+                const uint4 t = __ldcg(reinterpret_cast<const uint4*>(srow + gx));
+                v = *reinterpret_cast<const V*>(&t);
+            } else {
+                const unsigned int t = __ldcg(reinterpret_cast<const unsigned int*>(srow + gx));
+                v = *reinterpret_cast<const V*>(&t);
+            }
+            drow[c] = v;
+        }
+    }
+}
+
+template <int VEC>
+__device__ __forceinline__ void store_block(uint8_t* dst, const uint8_t* win, int L, int P, int bh, int bw, int ry0,
+                                            int rx0) {
+    using V = typename std::conditional<VEC == 16, uint4, uint32_t>::type;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int cpr = bw / VEC;
+    for (int y = warp; y < bh; y += nw) {
+        const V* srow = reinterpret_cast<const V*>(win + (kMargin + y) * P + kMarginX);
+        uint8_t* drow = dst + static_cast<size_t>(ry0 + y) * L + rx0;
+        for (int c = lane; c < cpr; c += 32) {
+            if (VEC == 16)
+                __stcg(reinterpret_cast<uint4*>(drow) + c, *reinterpret_cast<const uint4*>(srow + c));
+            else
+                __stcg(reinterpret_cast<unsigned int*>(drow) + c, *reinterpret_cast<const unsigned int*>(srow + c));
+        }
+    }
+}
+
 template <int ARITY>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int r = blockIdx.z;
     if (a.run.status[r] != kStatusRunning) return;
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1, M = kMargin;
+    const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
     const int ry0 = a.row_split[blockIdx.y], ry1 = a.row_split[blockIdx.y + 1];
     const int rx0 = a.col_split[blockIdx.x], rx1 = a.col_split[blockIdx.x + 1];
     const int bh = ry1 - ry0, bw = rx1 - rx0;
-    const int Wh = bh + 2 * M, Ww = bw + 2 * M;
+    const int Wh = bh + 2 * kMargin, Ww = bw + 2 * kMarginX;
     const size_t N = static_cast<size_t>(H) * L;
     const uint8_t* src = a.src + r * N;
     uint8_t* dst = a.dst + r * N;
     uint8_t* win = smem;
-    uint32_t* sT = reinterpret_cast<uint32_t*>(smem + align16(Wh * P));
-    uint32_t* sCnt = sT + S1 * S1;
+    const int woff = (Wh * P + 15) & ~15;
+    uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
+    int2* tblp = reinterpret_cast<int2*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15));
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(tblp + 32);
     __shared__ int sLast;
+    // 16-byte chunks when every window/block column boundary is 16-aligned in global memory
+    const bool v16 = (L & 15) == 0 && (rx0 & 15) == 0 && (bw & 15) == 0;
 
     if (a.step) {
-        const uint64_t seed = a.seeds[r];
-        const uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
-        const uint64_t mcs = static_cast<uint64_t>(a.mcs);
-        const int wy0 = ((ry0 - M) % H + H) % H;
-        const int wx0 = ((rx0 - M) % L + L) % L;
+        const uint32_t s32 = seed32(a.seeds[r]);
+        const int wy0 = ((ry0 - kMargin) % H + H) % H;
+        const int wx0 = ((rx0 - kMarginX) % L + L) % L;
         for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
-        {
-            const int wpr = Ww >> 2;
-            for (int idx = tid; idx < Wh * wpr; idx += nt) {
-                const int wr = idx / wpr, c = idx - (idx / wpr) * wpr;
-                const int gy = (wy0 + wr) % H;
-                const int gx = (wx0 + 4 * c) % L;
-                *reinterpret_cast<uint32_t*>(win + wr * P + 4 * c) =
-                    __ldcg(reinterpret_cast<const unsigned int*>(src + static_cast<size_t>(gy) * L + gx));
-            }
-        }
+        build_offset_table<ARITY>(tblp, P);
+        if (v16)
+            load_window<16>(win, src, H, L, P, Wh, Ww, wy0, wx0);
+        else
+            load_window<4>(win, src, H, L, P, Wh, Ww, wy0, wx0);
         __syncthreads();
-        const Rule R{a.rule.xm, a.rule.xi, a.rule.xm >> Bits<ARITY>::LB, a.rule.xi >> Bits<ARITY>::LB};
-        const Round rp = round_params(k0, k1, mcs);
-        const int Ty = H >> 1, Tx = L >> 1;
-        const int jb = wy0 >> 1, ib = wx0 >> 1;  // global tile index of window tile 0 (even)
-#pragma unroll 1
-        for (int p = 0; p < 4; ++p) {
-            const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-            const int lo = 3 * p, hiR = Wh - 3 * p, hiC = Ww - 3 * p;
-            // footprint rows [2j-oy-1, 2j-oy+2] within [lo, hiR)
-            const int jmin = (lo + rp.oy + 2) >> 1, jmax = (hiR - 3 + rp.oy) >> 1;
-            const int imin = (lo + rp.ox + 2) >> 1, imax = (hiC - 3 + rp.ox) >> 1;
-            const int j0 = jmin + ((jmin ^ cy) & 1), i0 = imin + ((imin ^ cx) & 1);
-            const int nj = jmax >= j0 ? ((jmax - j0) >> 1) + 1 : 0;
-            const int ni = imax >= i0 ? ((imax - i0) >> 1) + 1 : 0;
-            const int cnt = nj * ni;
-            if (tid < cnt) {
-                int aa = tid / ni, bb = tid - (tid / ni) * ni;
-                const int da = nt / ni, db = nt - (nt / ni) * ni;
-                const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p));
-                for (int k = tid; k < cnt; k += nt) {
-                    const int j = j0 + 2 * aa, i = i0 + 2 * bb;
-                    const int ty = (jb + j) % Ty, tx = (ib + i) % Tx;
-                    const uint32_t tile =
-                        static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(tx);
-                    const uint4 w = philox(tile, static_cast<uint32_t>(mcs), c2, 0u, k0, k1);
-                    tile_attempts<ARITY>(win, (2 * j - rp.oy) * P + (2 * i - rp.ox), P, w, R, sT, S1, k0, k1, tile,
-                                         mcs, p);
-                    bb += db;
-                    aa += da;
-                    if (bb >= ni) {
-                        bb -= ni;
-                        ++aa;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        {
-            const int wpr = bw >> 2;
-            for (int idx = tid; idx < bh * wpr; idx += nt) {
-                const int y = idx / wpr, c = idx - (idx / wpr) * wpr;
-                __stcg(reinterpret_cast<unsigned int*>(dst + static_cast<size_t>(ry0 + y) * L + rx0 + 4 * c),
-                       *reinterpret_cast<const uint32_t*>(win + (M + y) * P + M + 4 * c));
-            }
-        }
+        const uint32_t win0 = smem_addr(win), tbl = smem_addr(tblp), sTa = smem_addr(sT);
+        if (a.narrow)
+            block_phases<ARITY, true>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32, static_cast<uint64_t>(a.mcs));
+        else
+            block_phases<ARITY, false>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32, static_cast<uint64_t>(a.mcs));
+        if (v16)
+            store_block<16>(dst, win, L, P, bh, bw, ry0, rx0);
+        else
+            store_block<4>(dst, win, L, P, bh, bw, ry0, rx0);
     }
     if (a.count) {
         for (int v = tid; v < S1; v += nt) sCnt[v] = 0;
         __syncthreads();
         if (a.step)
-            block_count(win + M * P + M, bh, bw, P, S1, sCnt);
+            block_count(win + kMargin * P + kMarginX, bh, bw, P, S1, sCnt);
         else
             block_count(src + static_cast<size_t>(ry0) * L + rx0, bh, bw, L, S1, sCnt);
         __syncthreads();
@@ -372,14 +491,13 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         if (sLast && tid == 0) {
             __threadfence();
             uint64_t c64[kMaxSpecies + 1];
-            for (int v = 0; v < S1; ++v) {
-                c64[v] = atomicExch(&a.acc[r * S1 + v], 0ull);
-            }
+            for (int v = 0; v < S1; ++v) c64[v] = atomicExch(&a.acc[r * S1 + v], 0ull);
             a.ticket[r] = 0u;
             record_decide(c64, S1, a.mcs + a.step, r, a.run);
         }
     }
 }
+
 
 // ---------------------------------------------------------------------------------------------
 // Helpers
@@ -395,9 +513,7 @@ __global__ void init_kernel(InitArgs a) {
         const int r = static_cast<int>(t / pairs);
         const int64_t pi = t - static_cast<int64_t>(r) * pairs;
         uint8_t* lat = a.lat + static_cast<size_t>(r) * a.n;
-        const uint64_t seed = a.seeds[r];
-        const uint4 w = philox(static_cast<uint32_t>(pi), 0u, ctr2(0, kDomInit, 0u), 0u, static_cast<uint32_t>(seed),
-                               static_cast<uint32_t>(seed >> 32));
+        const uint4 w = philox(static_cast<uint32_t>(pi), 0u, ctr2(0, kDomInit, 0u, 0u), seed32(a.seeds[r]));
         const uint32_t S = static_cast<uint32_t>(a.S);
         for (int h = 0; h < 2; ++h) {
             const int64_t i = 2 * pi + h;
@@ -427,14 +543,12 @@ __global__ void count_kernel(const uint8_t* lat, int64_t n, int S1, unsigned lon
 // Serial replay of injected reference draws (engine.cpp:104-110) with the production rule.
 __global__ void replay_kernel(ReplayArgs a) {
     const uint32_t n = static_cast<uint32_t>(static_cast<int64_t>(a.H) * a.L);
-    const Rule R{a.rule.xm, a.rule.xi, a.rule.xm >> Bits<4>::LB, a.rule.xi >> Bits<4>::LB};
     const int S1 = a.S + 1;
     for (int64_t k = 0; k < a.n_attempts; ++k) {
         const uint32_t cell = a.wc[k] % n;
         const uint32_t d = a.wd[k] % static_cast<uint32_t>(a.arity);
-        const uint32_t word = a.wa[k];
         int dr, dc;
-        dir_rc<8>(d, dr, dc);
+        dir_rc(d, dr, dc);
         const int y = static_cast<int>(cell / static_cast<uint32_t>(a.L));
         const int x = static_cast<int>(cell % static_cast<uint32_t>(a.L));
         int ny = y + dr, nx = x + dc;
@@ -448,12 +562,10 @@ __global__ void replay_kernel(ReplayArgs a) {
             if (nx >= a.L) nx = 2 * (a.L - 1) - nx;
         }
         const int64_t ni = static_cast<int64_t>(ny) * a.L + nx;
-        const uint32_t s = a.lat[cell], nb = a.lat[ni];
-        uint32_t ns, nn;
-        // The refine functor returns the word's own low bits: every comparison sees the full word.
-        apply_rule<4>(s, nb, word, R, a.rule.T, S1, ns, nn, [&]() { return word & ((1u << Bits<4>::LB) - 1u); });
-        a.lat[cell] = static_cast<uint8_t>(ns);
-        a.lat[ni] = static_cast<uint8_t>(nn);
+        // the production rule with the injected full 32-bit action word
+        const uint32_t r = rule_exact(a.lat[cell], a.lat[ni], a.wa[k], a.rule.xm, a.rule.xi, a.rule.T, S1);
+        a.lat[cell] = static_cast<uint8_t>(r & 0xFFu);
+        a.lat[ni] = static_cast<uint8_t>(r >> 8);
     }
 }
 

@@ -9,7 +9,8 @@ namespace escgd {
 
 // Margin of the overlapped-tile (block) kernel: a tile footprint reaches 3 cells past the tile
 // origin, so validity shrinks by 3 cells per phase and 4 phases need 12 cells.
-constexpr int kMargin = 12;
+constexpr int kMargin = 12;   // rows
+constexpr int kMarginX = 16;  // columns: 12 + 4 so window column 0 stays 8-aligned (NARROW pairs)
 // Tile-kernel window: rows -2..H, cols -2..L (ghost frame of the periodic wrap), origin (2, 4).
 constexpr int kTileR0 = 2;
 constexpr int kTileC0 = 4;
@@ -42,6 +43,7 @@ struct TileArgs {
     RunArgs run;
     int H, L, S, P;   // P = shared-memory pitch
     int arity, flux;
+    int narrow;       // draw format
     int record;       // 1: record/check loop (escg_dev_run); 0: advance to run.mcs_limit
     int smem_bytes;
 };
@@ -54,6 +56,7 @@ struct BlockArgs {
     RunArgs run;
     int H, L, S, P;      // P = window pitch
     int arity;
+    int narrow;
     int nby, nbx;
     const int* row_split;  // nby+1 row boundaries (multiples of 4)
     const int* col_split;  // nbx+1

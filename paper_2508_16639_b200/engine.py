@@ -409,11 +409,18 @@ class DeviceEngine:
         check(lib().escg_dev_last_timing(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
+    def draw_format(self) -> str:
+        """'wide' or 'narrow' — which attempt-word layout this engine's draws use."""
+        v = C.c_int32(0)
+        check(lib().escg_dev_draw_format(self._h, C.byref(v)))
+        return "narrow" if v.value else "wide"
+
     def describe(self):
         vals = [C.c_int32(0) for _ in range(4)]
         check(lib().escg_dev_describe(self._h, *[C.byref(v) for v in vals]))
         kernel, ctas, threads, smem = (v.value for v in vals)
-        return dict(kernel={1: "tile", 2: "block"}[kernel], ctas=ctas, threads=threads, smem_bytes=smem)
+        return dict(kernel={1: "tile", 2: "block"}[kernel], ctas=ctas, threads=threads, smem_bytes=smem,
+                    draw_format=self.draw_format())
 
 
 def thresholds(mobility: float, cells: int, model: DominanceModel):

@@ -117,26 +117,48 @@ def test_tile_kernel_matches_crs_oracle(escg, oracle, case):
         got3 = eng.get_lattice()
         eng.advance(4)
         got7 = eng.get_lattice()
-    want3 = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 3, arity=arity, flux=flux)
+        narrow = eng.draw_format() == "narrow"
+    want3 = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 3, arity=arity, flux=flux, narrow=narrow)
     assert np.array_equal(got3, want3)
-    want7 = oracle.crs_run(want3, L, H, model.matrix(), M, seed, 3, 4, arity=arity, flux=flux)
+    want7 = oracle.crs_run(want3, L, H, model.matrix(), M, seed, 3, 4, arity=arity, flux=flux, narrow=narrow)
     assert np.array_equal(got7, want7)
 
 
-@pytest.mark.parametrize("LH", [(64, 64), (200, 200), (96, 160), (8, 8)])
+@pytest.mark.parametrize("fmt", ["wide", "narrow"])
+@pytest.mark.parametrize("LH", [(64, 64), (200, 200), (96, 160), (8, 8), (100, 36)])
 @pytest.mark.parametrize("arity", [4, 8])
-def test_block_kernel_matches_crs_oracle(escg, oracle, LH, arity):
+def test_block_kernel_matches_crs_oracle(escg, oracle, LH, arity, fmt, monkeypatch):
     L, H = LH
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", fmt)
     model = escg.make_circulant(3, [1])
     seed = 99
-    p = params(escg, L, H, 3, 1e-3, 0.1, arity, True, seed=seed)
+    M = 1e-2 if fmt == "narrow" else 1e-3
+    p = params(escg, L, H, 3, M, 0.1, arity, True, seed=seed)
     with escg.DeviceEngine(p, model, kernel="block") as eng:
         eng.init_lattice()
         init = eng.get_lattice()
         eng.advance(5)
         got = eng.get_lattice()
-    want = oracle.crs_run(init, L, H, model.matrix(), 1e-3, seed, 0, 5, arity=arity)
+        narrow = eng.draw_format() == "narrow"
+    assert narrow == (fmt == "narrow" and L % 8 == 0)
+    want = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 5, arity=arity, narrow=narrow)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("LH", [(64, 64), (200, 200), (96, 160), (8, 8)])
+def test_tile_kernel_narrow_matches_crs_oracle(escg, oracle, LH, monkeypatch):
+    L, H = LH
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "narrow")
+    model = escg.make_rpsls()
+    seed = 4242
+    p = params(escg, L, H, 5, 3e-3, 0.0, 4, True, seed=seed)
+    with escg.DeviceEngine(p, model, kernel="tile") as eng:
+        assert eng.draw_format() == "narrow"
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(6)
+        got = eng.get_lattice()
+    assert np.array_equal(got, oracle.crs_run(init, L, H, model.matrix(), 3e-3, seed, 0, 6, narrow=True))
 
 
 def test_block_equals_tile_kernel(escg):
@@ -167,7 +189,8 @@ def test_run_records_and_stop_rules(escg, oracle, kernel):
         assert st[0] == escg.RunStatus.Completed
         assert steps.tolist() == [0, 5, 10, 15, 20, 23]
         assert eng.mcs() == 23
-    want = oracle.crs_run(init, L, L, model.matrix(), 1e-4, 5, 0, 23)
+        narrow = eng.draw_format() == "narrow"
+    want = oracle.crs_run(init, L, L, model.matrix(), 1e-4, 5, 0, 23, narrow=narrow)
     assert np.array_equal(final, want)
     assert np.array_equal(counts[-1], oracle.densities(want, 3))
     assert np.array_equal(counts[0], oracle.densities(init, 3))
@@ -185,10 +208,11 @@ def test_tracked_extinction_stops_like_on_record(escg, oracle):
         steps, counts = eng.read_trace()
         t = eng.mcs()
         final = eng.get_lattice()
+        narrow = eng.draw_format() == "narrow"
     assert st[0] == escg.RunStatus.Stopped
     assert counts[-1][4] == 0 and all(c[4] > 0 for c in counts[:-1])
     assert steps[-1] == t
-    assert np.array_equal(final, oracle.crs_run(init, L, L, model.matrix(), 3e-5, 3, 0, t))
+    assert np.array_equal(final, oracle.crs_run(init, L, L, model.matrix(), 3e-5, 3, 0, t, narrow=narrow))
 
 
 def test_replicas_equal_single_runs(escg):

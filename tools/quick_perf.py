@@ -19,7 +19,7 @@ def probe(L, n_mcs, kernel="auto", reps=1, M=1e-4, p0=0.1, S=3):
         ms, launches = eng.last_timing()
         d = eng.describe()
     att = L * L * n_mcs * reps / (ms / 1e3)
-    return dict(L=L, reps=reps, kernel=d["kernel"], ctas=d["ctas"], smem=d["smem_bytes"], mcs=n_mcs, ms=ms,
+    return dict(L=L, reps=reps, fmt=d["draw_format"], kernel=d["kernel"], ctas=d["ctas"], smem=d["smem_bytes"], mcs=n_mcs, ms=ms,
                 wall_ms=wall * 1e3, launches=launches, attempts_per_s=att, mcs_per_s=n_mcs / (ms / 1e3),
                 hbm_frac=att * 2 / 6537.3e9)
 
