@@ -10,7 +10,7 @@ import numpy as np
 from .errors import raise_for
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libescg_b200.so")
+LIB_PATH = os.environ.get("ESCG_LIB") or os.path.join(PKG, "libescg_b200.so")
 
 ESCG_KERNEL_AUTO, ESCG_KERNEL_TILE, ESCG_KERNEL_BLOCK = 0, 1, 2
 ESCG_STOP_TRACKED, ESCG_STOP_STASIS = 1, 2

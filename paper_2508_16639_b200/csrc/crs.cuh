@@ -17,6 +17,10 @@ constexpr uint32_t kKey0 = 0xA4093822u, kKey1 = 0x299F31D0u;
 // Philox4x32-10 (Salmon et al. SC'11) with the fixed key: every round key is an immediate, so a
 // round is 2 IMAD.WIDE.U32 + 2 LOP3.
 __device__ __forceinline__ uint4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3) {
+#ifdef ESCG_DIAG_CHEAP_RNG  // diagnostic builds only (tools/ablate.py): not a valid generator
+    const uint32_t h = (c0 * 0x9E3779B9u) ^ (c1 * 0x85EBCA6Bu) ^ c2 ^ c3;
+    return make_uint4(h, h * 0xC2B2AE35u, h ^ 0x27D4EB2Fu, h * 0x165667B1u);
+#endif
     uint32_t k0 = kKey0, k1 = kKey1;
 #pragma unroll
     for (int r = 0; r < 10; ++r) {
@@ -278,6 +282,95 @@ __device__ __forceinline__ void tile_narrow(uint32_t wa, uint32_t wb, uint32_t b
     attempt<ARITY, true>(wa >> 16, base, tile, 1, C);
     attempt<ARITY, true>(wb & 0xFFFFu, base, tile, 2, C);
     attempt<ARITY, true>(wb >> 16, base, tile, 3, C);
+}
+
+// Exchange the pair (a <- vb, b <- va) unless the values are equal (predicated, no branch).
+__device__ __forceinline__ void swap_store(uint32_t a, uint32_t b, uint32_t va, uint32_t vb) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %2, %3;\n\t@p st.shared.u8 [%0], %3;\n\t@p st.shared.u8 [%1], %2;\n\t}" ::"r"(a),
+        "r"(b), "r"(va), "r"(vb));
+}
+
+// Store a rule result r = ns | nn << 8 unless the pair was equal (engine.hpp:113: no change).
+__device__ __forceinline__ void result_store(uint32_t a, uint32_t b, uint32_t s, uint32_t n, uint32_t r) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t.reg .b32 t0, t1;\n\tsetp.ne.u32 p, %2, %3;\n\tand.b32 t0, %4, 255;\n\tshr.u32 t1, %4, 8;\n\t"
+        "@p st.shared.u8 [%0], t0;\n\t@p st.shared.u8 [%1], t1;\n\t}" ::"r"(a),
+        "r"(b), "r"(s), "r"(n), "r"(r));
+}
+
+// Two disjoint tiles A and B of the same phase, their 4 attempts interleaved (A0 B0 A1 B1 ...):
+// each tile's attempts stay in order, the two chains overlap their shared-memory latencies.
+// NARROW: bits are 16-bit halves; WIDE: 32-bit words.
+template <int ARITY, bool NARROW>
+__device__ __forceinline__ void tile_dual_ordered(const uint32_t (&bA)[4], uint32_t baseA, uint32_t tA,
+                                                  const uint32_t (&bB)[4], uint32_t baseB, uint32_t tB,
+                                                  const PhaseCtx& C) {
+#ifdef ESCG_DIAG_NO_ATTEMPTS  // diagnostic: keep the draws live, skip the attempts
+    if ((bA[0] ^ bA[1] ^ bA[2] ^ bA[3] ^ bB[0] ^ bB[1] ^ bB[2] ^ bB[3]) == 0x12345u) sts8(baseA, tA);
+    return;
+#endif
+    constexpr uint32_t M = Bits<ARITY>::NT - 1;
+    uint2 oA = lds64(C.tbl + ((bA[0] & M) << 3)), oB = lds64(C.tbl + ((bB[0] & M) << 3));
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const uint32_t saA = baseA + oA.x, naA = baseA + oA.y, saB = baseB + oB.x, naB = baseB + oB.y;
+        const uint32_t sA = lds8(saA), nA = lds8(naA), sB = lds8(saB), nB = lds8(naB);
+        if (a < 3) {  // next attempt's offsets do not depend on the lattice
+            oA = lds64(C.tbl + ((bA[a + 1] & M) << 3));
+            oB = lds64(C.tbl + ((bB[a + 1] & M) << 3));
+        }
+        if (NARROW) {
+            const bool fA = bA[a] < C.fast, fB = bB[a] < C.fast;
+            if (fA & fB) {  // both certain migrations (engine.hpp:118-122)
+                swap_store(saA, naA, sA, nA);
+                swap_store(saB, naB, sB, nB);
+            } else {
+                const uint32_t rA =
+                    fA ? (nA | (sA << 8))
+                       : slow_narrow<ARITY>(sA, nA, bA[a], tA, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+                const uint32_t rB =
+                    fB ? (nB | (sB << 8))
+                       : slow_narrow<ARITY>(sB, nB, bB[a], tB, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+                result_store(saA, naA, sA, nA, rA);
+                result_store(saB, naB, sB, nB, rB);
+            }
+        } else {
+            const uint32_t rA = rule_wide<ARITY>(sA, nA, bA[a], tA, a, C);
+            const uint32_t rB = rule_wide<ARITY>(sB, nB, bB[a], tB, a, C);
+            result_store(saA, naA, sA, nA, rA);
+            result_store(saB, naB, sB, nB, rB);
+        }
+    }
+}
+
+// The upper half-warp runs B's chain first: with a window pitch ≡ 0 (mod 128 bytes) the two
+// half-warps then touch the even and the odd banks (DESIGN.md §Shared-memory layout).
+template <int ARITY, bool NARROW>
+__device__ __forceinline__ void tile_dual(const uint32_t (&bA)[4], uint32_t baseA, uint32_t tA, const uint32_t (&bB)[4],
+                                          uint32_t baseB, uint32_t tB, const PhaseCtx& C) {
+    const bool sw = (threadIdx.x & 16) != 0;  // data swap (selects), not divergent control flow
+    const uint32_t b1[4] = {sw ? bB[0] : bA[0], sw ? bB[1] : bA[1], sw ? bB[2] : bA[2], sw ? bB[3] : bA[3]};
+    const uint32_t b2[4] = {sw ? bA[0] : bB[0], sw ? bA[1] : bB[1], sw ? bA[2] : bB[2], sw ? bA[3] : bB[3]};
+    tile_dual_ordered<ARITY, NARROW>(b1, sw ? baseB : baseA, sw ? tB : tA, b2, sw ? baseA : baseB, sw ? tA : tB, C);
+}
+
+// NARROW pair draw → both tiles, interleaved.
+template <int ARITY>
+__device__ __forceinline__ void pair_narrow(const uint4 w, uint32_t baseA, uint32_t tA, uint32_t baseB, uint32_t tB,
+                                            const PhaseCtx& C) {
+    const uint32_t bA[4] = {w.x & 0xFFFFu, w.x >> 16, w.y & 0xFFFFu, w.y >> 16};
+    const uint32_t bB[4] = {w.z & 0xFFFFu, w.z >> 16, w.w & 0xFFFFu, w.w >> 16};
+    tile_dual<ARITY, true>(bA, baseA, tA, bB, baseB, tB, C);
+}
+
+// Two WIDE tiles with their own draws, interleaved.
+template <int ARITY>
+__device__ __forceinline__ void pair_wide(const uint4 wA, uint32_t baseA, uint32_t tA, const uint4 wB, uint32_t baseB,
+                                          uint32_t tB, const PhaseCtx& C) {
+    const uint32_t bA[4] = {wA.x, wA.y, wA.z, wA.w};
+    const uint32_t bB[4] = {wB.x, wB.y, wB.z, wB.w};
+    tile_dual<ARITY, false>(bA, baseA, tA, bB, baseB, tB, C);
 }
 
 // Mirror-reflect variant (flux=false, lattice.hpp:42-47; WIDE format only): tile cells outside the

@@ -182,6 +182,7 @@ struct escg_dev {
     int P = 0;
     int nby = 1, nbx = 1;
     int narrow = 0;  // draw format
+    int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     Thresholds th;
@@ -198,6 +199,7 @@ struct escg_dev {
     DevBuf<unsigned long long> d_acc;
     DevBuf<unsigned int> d_ticket;
     DevBuf<int> d_rows, d_cols, d_bad;
+    DevBuf<int32_t> d_cur;
     DevBuf<int32_t> d_i32;
     int64_t trace_cap = 0;
     bool traced = false;
@@ -215,42 +217,51 @@ namespace {
 
 // Block-kernel decomposition: row splits at multiples of 4, column splits at multiples of 8 when
 // L % 8 == 0 (keeps NARROW tile pairs aligned), minimising waves x computed window area.
-size_t block_smem(int bh, int bw, int S1, int* pitch) {
-    const int P = ((bw + 2 * escgd::kMarginX) + 15) & ~15;
+size_t block_smem(int bh, int bw, int S1, int k, int* pitch) {
+    // pitch ≡ 0 (mod 128 bytes): see tile_dual (bank-conflict-light half-warp split)
+    const int P = ((bw + 2 * escgd::margin_cols(k)) + 127) & ~127;
     if (pitch) *pitch = P;
-    return static_cast<size_t>((((bh + 2 * escgd::kMargin) * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8 +
-                               (escgd::kMaxSpecies + 1) * 4 + 64);
+    return static_cast<size_t>((((bh + 2 * escgd::margin_rows(k)) * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) +
+                               32 * 8 + (escgd::kMaxSpecies + 1) * 4 + 64);
 }
 
-void plan_blocks(escg_dev* h, int sms, int smem_cap) {
+// Block-kernel decomposition: row splits at multiples of 4, column splits at multiples of 16 (8, 4)
+// when L allows (TMA rows, NARROW pairs), and k MCS per launch (temporal blocking).  Model per MCS:
+// waves x (mean valid area over the 4k phases + launch/load overhead / k), in cell units.
+void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     const int cu = (h->L % 16 == 0) ? 16 : ((h->L % 8 == 0) ? 8 : 4);
     const int uy = h->H / 4, ux = h->L / cu;
     double best = 1e300;
-    int bnby = 1, bnbx = 1;
-    for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
-        for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
-            const int bh = ((uy + nby - 1) / nby) * 4, bw = ((ux + nbx - 1) / nbx) * cu;
-            if (block_smem(bh, bw, h->S1, nullptr) > static_cast<size_t>(smem_cap)) continue;
-            const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
-            const int64_t waves = (ctas + sms - 1) / sms;
-            // compute ∝ average valid area over the 4 phases (12-cell margin → ~6 extra per side)
-            const double cost = static_cast<double>(waves) * (bh + 12.0) * (bw + 12.0) + 2000.0 * waves;
-            if (cost < best) {
-                best = cost;
-                bnby = nby;
-                bnbx = nbx;
+    int bnby = 1, bnbx = 1, bk = 1;
+    const double kOverheadCells = 40000.0;  // launch + window load/store, measured on B200
+    for (int k = 1; k <= kmax; ++k) {
+        for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
+            for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
+                const int bh = ((uy + nby - 1) / nby) * 4, bw = ((ux + nbx - 1) / nbx) * cu;
+                if (block_smem(bh, bw, h->S1, k, nullptr) > static_cast<size_t>(smem_cap)) continue;
+                const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
+                const int64_t waves = (ctas + sms - 1) / sms;
+                const double area = (bh + 12.0 * k + 3.0) * (bw + 12.0 * k + 3.0);
+                const double cost = static_cast<double>(waves) * (area + kOverheadCells / k);
+                if (cost < best * 0.999) {
+                    best = cost;
+                    bnby = nby;
+                    bnbx = nbx;
+                    bk = k;
+                }
             }
         }
     }
     h->nby = bnby;
     h->nbx = bnbx;
+    h->kmcs = bk;
     std::vector<int> rows(bnby + 1), cols(bnbx + 1);
     for (int i = 0; i <= bnby; ++i) rows[i] = static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
     for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(ux) * i / bnbx) * cu;
     int bh = 0, bw = 0;
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
-    h->smem = static_cast<int>(block_smem(bh, bw, h->S1, &h->P));
+    h->smem = static_cast<int>(block_smem(bh, bw, h->S1, bk, &h->P));
     h->d_rows.alloc(rows.size());
     h->d_cols.alloc(cols.size());
     CK(cudaMemcpy(h->d_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
@@ -268,6 +279,7 @@ escgd::RunArgs run_args(escg_dev* h, int64_t limit, int64_t interval, uint32_t f
     r.trace_steps = trace ? h->d_tsteps.p : nullptr;
     r.trace_counts = trace ? h->d_tcounts.p : nullptr;
     r.trace_cap = trace ? h->trace_cap : 0;
+    r.cur = h->d_cur.p;
     r.mcs_limit = limit;
     r.interval = interval;
     r.stop_flags = flags;
@@ -311,9 +323,10 @@ void timed_end(escg_dev* h, int64_t launches) {
     h->last_launches = launches;
 }
 
-// Block path: enqueue MCS [t, t+n) with records at the end when `record_last`.
+// Block path: enqueue MCS [t, t+n) in launches of at most kmcs MCS, density record after the
+// last one when `count_last`.  `launch_no` counts launches since the run start (buffer parity).
 int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, const escgd::RunArgs& run,
-                            int64_t t0) {
+                            int64_t& launch_no) {
     escgd::BlockArgs a{};
     a.seeds = h->d_seeds.p;
     a.rule = rule_args(h);
@@ -332,16 +345,22 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.ticket = h->d_ticket.p;
     a.smem_bytes = h->smem;
     a.step = 1;
-    for (int64_t k = 0; k < n; ++k) {
-        const int64_t m = t + k;
-        const int par = static_cast<int>((m - t0) & 1);
+    int64_t launches = 0;
+    for (int64_t done = 0; done < n;) {
+        const int k = static_cast<int>(std::min<int64_t>(h->kmcs, n - done));
+        const int par = static_cast<int>(launch_no & 1);
         a.src = h->lat[par].p;
         a.dst = h->lat[1 - par].p;
-        a.mcs = m;
-        a.count = (count_last && k == n - 1) ? 1 : 0;
+        a.dst_index = 1 - par;
+        a.mcs = t + done;
+        a.nmcs = k;
+        done += k;
+        a.count = (count_last && done == n) ? 1 : 0;
         CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
+        ++launch_no;
+        ++launches;
     }
-    return n;
+    return launches;
 }
 
 void ensure_trace(escg_dev* h, int64_t records) {
@@ -393,6 +412,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         CK(cudaMemsetAsync(h->d_acc.p, 0, sizeof(unsigned long long) * h->S1 * h->nrep, h->stream));
         CK(cudaMemsetAsync(h->d_ticket.p, 0, sizeof(unsigned int) * h->nrep, h->stream));
         const int64_t t0 = h->mcs[0];
+        int64_t launch_no = 0;
         // record at the starting MCS (record_and_check before any step, engine.cpp:181)
         escgd::BlockArgs a{};
         a.src = h->lat[0].p;
@@ -411,6 +431,8 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.row_split = h->d_rows.p;
         a.col_split = h->d_cols.p;
         a.mcs = t0;
+        a.nmcs = 1;
+        a.dst_index = 1;  // count-only: the lattice stays in buffer 0
         a.step = 0;
         a.count = 1;
         a.acc = h->d_acc.p;
@@ -429,7 +451,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         const int64_t kChunk = 512;
         while (t < limit) {
             const int64_t adv = std::min(interval, limit - t);
-            launches += enqueue_block_steps(h, t, adv, true, run, t0);
+            launches += enqueue_block_steps(h, t, adv, true, run, launch_no);
             t += adv;
             since_poll += adv;
             if (since_poll >= kChunk) {
@@ -594,7 +616,10 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
             h->threads = 512;
         } else {
             h->lat[1].alloc(static_cast<size_t>(h->N) * n_replicas);
-            plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024));
+            int kmax = escgd::kMaxBlockMcs;
+            if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
+            plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
+            h->d_cur.alloc(n_replicas);
             h->threads = 1024;
             h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
             h->d_ticket.alloc(n_replicas);
@@ -729,12 +754,13 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
             const escgd::RunArgs run = run_args(h, 0, 1, 0, 0, false);
             CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t) * h->nrep, h->stream));
             const int64_t t0 = h->mcs[0];
+            int64_t launch_no = 0;
             timed_begin(h);
-            launches = enqueue_block_steps(h, t0, n_mcs, false, run, t0);
+            launches = enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
             timed_end(h, launches);
             for (int r = 0; r < h->nrep; ++r) {
                 h->mcs[r] += n_mcs;
-                h->cur[r] = static_cast<int>(n_mcs & 1);
+                h->cur[r] = static_cast<int>(launch_no & 1);
             }
         }
         CK(cudaGetLastError());
@@ -748,8 +774,9 @@ int escg_dev_run(escg_dev* h, int64_t mcs_limit, int64_t interval, uint32_t stop
         CK(cudaSetDevice(h->device));
         const std::vector<int64_t> start(h->mcs);
         run_impl(h, mcs_limit, interval, stop_flags, tracked_species, record_trace != 0, status_out);
+        (void)start;
         if (h->kernel == ESCG_KERNEL_BLOCK)
-            for (int r = 0; r < h->nrep; ++r) h->cur[r] = static_cast<int>((h->mcs[r] - start[r]) & 1);
+            CK(cudaMemcpy(h->cur.data(), h->d_cur.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost));
     });
 }
 

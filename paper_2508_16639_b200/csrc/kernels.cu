@@ -18,7 +18,26 @@
 
 namespace escgd {
 
+#ifdef ESCG_DIAG_TIMING
+// diagnostic builds only: per-CTA %globaltimer stamps of the block kernel's sections
+__device__ unsigned long long g_diag_t[4096 * 16];
+#endif
+
 namespace {
+
+#ifdef ESCG_DIAG_TIMING
+__device__ __forceinline__ void diag_stamp(int slot) {
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        const int cta = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+        if (cta < 4096) g_diag_t[cta * 16 + slot] = t;
+    }
+}
+#define DIAG_STAMP(s) diag_stamp(s)
+#else
+#define DIAG_STAMP(s)
+#endif
 
 constexpr int kStatusRunning = -1;
 constexpr int kCompleted = 0, kStasis = 1, kStopped = 2;
@@ -177,31 +196,36 @@ __device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t 
         const PhaseCtx C = phase_ctx<ARITY>(rule, narrow, tbl, sT, S1, mcs, p, s32);
         const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
         const int nty = (Ty - cy + 1) >> 1;
-        // items: tiles (WIDE) or tile pairs (NARROW, periodic with L % 8 == 0) of this colour
-        const int nxi = (!REFLECT && narrow) ? (Tx >> 2) : ((Tx - cx + 1) >> 1);
+        const int ntx = (Tx - cx + 1) >> 1;  // tiles of this colour per tile row
+        // items: pairs of same-colour tiles (tx, tx+2) of a row (one NARROW draw, or two WIDE
+        // draws, per pair; the last item of a row may hold one tile), single tiles when reflecting
+        const int nxi = REFLECT ? ntx : ((ntx + 1) >> 1);
         const int cnt = nty * nxi;
         if (tid < cnt) {
             int i = udiv_small(tid, nxi), j = tid - udiv_small(tid, nxi) * nxi;
             const int di = udiv_small(nt, nxi), dj = nt - udiv_small(nt, nxi) * nxi;
             for (int k = tid; k < cnt; k += nt) {
                 const int ty = cy + 2 * i;
-                if (!REFLECT && narrow) {
-                    const uint32_t pair = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx >> 2) + j;
-                    const uint4 w = philox(pair, C.c1, c2, s32);
-                    const int tx0 = cx + 4 * j;
-                    const uint32_t row = lat0 + static_cast<uint32_t>((2 * ty - rp.oy + kTileR0) * P + kTileC0 - rp.ox);
-                    const uint32_t t0 = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + tx0;
-                    tile_narrow<ARITY>(w.x, w.y, row + 2 * tx0, t0, C);
-                    tile_narrow<ARITY>(w.z, w.w, row + 2 * tx0 + 4, t0 + 2, C);
-                } else {
+                if (REFLECT) {
                     const int tx = cx + 2 * j;
                     const uint32_t tile = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(tx);
                     const uint4 w = philox(tile, C.c1, c2, s32);
-                    if (REFLECT)
-                        tile_reflect<ARITY>(w, lat0, 2 * ty - rp.oy, 2 * tx - rp.ox, kTileR0, kTileC0, P, H, L, tile, C);
-                    else
-                        tile_wide<ARITY>(w, lat0 + static_cast<uint32_t>((2 * ty - rp.oy + kTileR0) * P + 2 * tx - rp.ox + kTileC0),
-                                         tile, C);
+                    tile_reflect<ARITY>(w, lat0, 2 * ty - rp.oy, 2 * tx - rp.ox, kTileR0, kTileC0, P, H, L, tile, C);
+                } else {
+                    const int tx0 = cx + 4 * j;
+                    const uint32_t row = lat0 + static_cast<uint32_t>((2 * ty - rp.oy + kTileR0) * P + kTileC0 - rp.ox);
+                    const uint32_t t0 = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + tx0;
+                    const uint32_t b0 = row + 2 * tx0;
+                    const bool two = 2 * j + 1 < ntx;
+                    if (narrow) {  // L % 8 == 0: every pair is complete
+                        const uint4 w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx >> 2) + j, C.c1, c2, s32);
+                        pair_narrow<ARITY>(w, b0, t0, b0 + 4, t0 + 2, C);
+                    } else if (two) {
+                        const uint4 wA = philox(t0, C.c1, c2, s32), wB = philox(t0 + 2, C.c1, c2, s32);
+                        pair_wide<ARITY>(wA, b0, t0, wB, b0 + 4, t0 + 2, C);
+                    } else {
+                        tile_wide<ARITY>(philox(t0, C.c1, c2, s32), b0, t0, C);
+                    }
                 }
                 j += dj;
                 i += di;
@@ -252,7 +276,7 @@ __device__ void tile_copy(uint8_t* lat, uint8_t* glat, int H, int L, int P) {
 }
 
 template <int ARITY, bool REFLECT>
-__global__ void __launch_bounds__(512) tile_kernel(TileArgs a) {
+__global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
     const TileSmem lay = tile_layout(H, L, a.S, P);
@@ -318,70 +342,120 @@ __device__ __forceinline__ int wrap_down(int v, int n, bool big) {
 
 template <int ARITY, bool NARROW>
 __device__ __forceinline__ void block_phases(const BlockArgs& a, uint32_t win0, uint32_t tbl, uint32_t sT, int S1,
-                                             int Wh, int Ww, int wy0, int wx0, uint32_t s32, uint64_t mcs) {
+                                             int Wh, int Ww, int wy0, int wx0, uint32_t s32) {
     const int tid = threadIdx.x, nt = blockDim.x, P = a.P;
-    const Round rp = round_params(s32, mcs);
     const int Ty = a.H >> 1, Tx = a.L >> 1, TQ = a.L >> 3;
     const int jb = wy0 >> 1, ib = wx0 >> 1;  // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
-    const int ex = kMarginX - kMargin;        // extra loaded columns beyond the 12-cell margin
-    const bool big = Wh > a.H || Ww > a.L;    // window wraps more than once: use a true modulo
+    const int ex = margin_cols(a.nmcs) - margin_rows(a.nmcs);  // extra loaded columns
+    const bool big = Wh > a.H || Ww > a.L;  // window wraps more than once: use a true modulo
 #pragma unroll 1
-    for (int p = 0; p < 4; ++p) {
-        const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-        const PhaseCtx C = phase_ctx<ARITY>(a.rule, NARROW, tbl, sT, S1, mcs, p, s32);
-        const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
-        // footprint rows [2j-oy-1, 2j-oy+2] within [3p, Wh-3p); cols likewise within [ex+3p, Ww-ex-3p)
-        const int lo = 3 * p, hiR = Wh - 3 * p, loC = ex + 3 * p, hiC = Ww - ex - 3 * p;
-        const int jmin = (lo + rp.oy + 2) >> 1, jmax = (hiR - 3 + rp.oy) >> 1;
-        const int imin = (loC + rp.ox + 2) >> 1, imax = (hiC - 3 + rp.ox) >> 1;
-        const int j0 = jmin + ((jmin ^ cy) & 1);
-        const int nj = jmax >= j0 ? ((jmax - j0) >> 1) + 1 : 0;
-        int u0, nu;
-        if (NARROW) {
-            u0 = (imin - cx + 1) >> 2;
-            const int u1 = imax >= cx ? (imax - cx) >> 2 : -1;
-            nu = u1 >= u0 ? u1 - u0 + 1 : 0;
-        } else {
-            u0 = imin + ((imin ^ cx) & 1);
-            nu = imax >= u0 ? ((imax - u0) >> 1) + 1 : 0;
-        }
-        const int cnt = nj * nu;
-        if (tid < cnt) {
-            const int q0 = udiv_small(tid, nu), qn = udiv_small(nt, nu);
-            int aa = q0, bb = tid - q0 * nu;
-            const int da = qn, db = nt - qn * nu;
-            for (int k = tid; k < cnt; k += nt) {
-                const int j = j0 + 2 * aa;
-                const int ty = wrap_down(jb + j, Ty, big);
-                const uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
-                if (NARROW) {
-                    const int u = u0 + bb;
-                    const int q = wrap_down((ib >> 2) + u, TQ, big);
-                    const uint4 w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(TQ) + q, C.c1, c2, s32);
-                    const int i0 = cx + 4 * u;
-                    const uint32_t t0 = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + 4 * q + cx;
-                    if (i0 >= imin && i0 <= imax) tile_narrow<ARITY>(w.x, w.y, rowbase + 2 * i0, t0, C);
-                    if (i0 + 2 >= imin && i0 + 2 <= imax) tile_narrow<ARITY>(w.z, w.w, rowbase + 2 * i0 + 4, t0 + 2, C);
-                } else {
-                    const int i = u0 + 2 * bb;
-                    const int tx = wrap_down(ib + i, Tx, big);
-                    const uint32_t tile = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(tx);
-                    const uint4 w = philox(tile, C.c1, c2, s32);
-                    tile_wide<ARITY>(w, rowbase + 2 * i, tile, C);
-                }
-                bb += db;
-                aa += da;
-                if (bb >= nu) {
-                    bb -= nu;
-                    ++aa;
+    for (int t = 0; t < a.nmcs; ++t) {
+        const uint64_t mcs = static_cast<uint64_t>(a.mcs + t);
+        const Round rp = round_params(s32, mcs);
+#pragma unroll 1
+        for (int p = 0; p < 4; ++p) {
+            const int q = 4 * t + p;  // global phase of this launch: validity shrinks 3 cells per phase
+            const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
+            const PhaseCtx C = phase_ctx<ARITY>(a.rule, NARROW, tbl, sT, S1, mcs, p, s32);
+            const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+            // footprint rows [2j-oy-1, 2j-oy+2] within [3q, Wh-3q); cols within [ex+3q, Ww-ex-3q)
+            const int lo = 3 * q, hiR = Wh - 3 * q, loC = ex + 3 * q, hiC = Ww - ex - 3 * q;
+            const int jmin = (lo + rp.oy + 2) >> 1, jmax = (hiR - 3 + rp.oy) >> 1;
+            const int imin = (loC + rp.ox + 2) >> 1, imax = (hiC - 3 + rp.ox) >> 1;
+            const int j0 = jmin + ((jmin ^ cy) & 1);
+            const int nj = jmax >= j0 ? ((jmax - j0) >> 1) + 1 : 0;
+            // items: pairs of same-colour tiles (i, i+2).  NARROW pairs are the global draw pairs
+            // (window column 0 is 8-aligned); WIDE pairs are local.  Edge items may hold one tile.
+            const int i0 = imin + ((imin ^ cx) & 1);  // first valid tile column of this colour
+            int u0, nu;
+            if (NARROW) {
+                u0 = (imin - cx + 1) >> 2;
+                const int u1 = imax >= cx ? (imax - cx) >> 2 : -1;
+                nu = u1 >= u0 ? u1 - u0 + 1 : 0;
+            } else {
+                const int ni = imax >= i0 ? ((imax - i0) >> 1) + 1 : 0;
+                u0 = 0;
+                nu = (ni + 1) >> 1;
+            }
+            const int cnt = nj * nu;
+            if (tid < cnt) {
+                const int q0 = udiv_small(tid, nu), qn = udiv_small(nt, nu);
+                int aa = q0, bb = tid - q0 * nu;
+                const int da = qn, db = nt - qn * nu;
+                for (int k = tid; k < cnt; k += nt) {
+                    const int j = j0 + 2 * aa;
+                    const int ty = wrap_down(jb + j, Ty, big);
+                    const uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
+                    const uint32_t trow = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx);
+                    if (NARROW) {
+                        const int u = u0 + bb;
+                        const int qq = wrap_down((ib >> 2) + u, TQ, big);
+                        const uint4 w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(TQ) + qq, C.c1, c2, s32);
+                        const int ia = cx + 4 * u;
+                        const uint32_t t0 = trow + 4 * qq + cx;
+                        const bool okA = ia >= imin && ia <= imax, okB = ia + 2 >= imin && ia + 2 <= imax;
+                        if (okA & okB) {
+                            pair_narrow<ARITY>(w, rowbase + 2 * ia, t0, rowbase + 2 * ia + 4, t0 + 2, C);
+                        } else {
+                            if (okA) tile_narrow<ARITY>(w.x, w.y, rowbase + 2 * ia, t0, C);
+                            if (okB) tile_narrow<ARITY>(w.z, w.w, rowbase + 2 * ia + 4, t0 + 2, C);
+                        }
+                    } else {
+                        const int ia = i0 + 4 * bb;
+                        const uint32_t tA = trow + wrap_down(ib + ia, Tx, big);
+                        const uint4 wA = philox(tA, C.c1, c2, s32);
+                        if (ia + 2 <= imax) {
+                            const uint32_t tB = trow + wrap_down(ib + ia + 2, Tx, big);
+                            pair_wide<ARITY>(wA, rowbase + 2 * ia, tA, philox(tB, C.c1, c2, s32), rowbase + 2 * ia + 4,
+                                             tB, C);
+                        } else {
+                            tile_wide<ARITY>(wA, rowbase + 2 * ia, tA, C);
+                        }
+                    }
+                    bb += db;
+                    aa += da;
+                    if (bb >= nu) {
+                        bb -= nu;
+                        ++aa;
+                    }
                 }
             }
+#ifndef ESCG_DIAG_NO_PHASE_SYNC
+            __syncthreads();
+#endif
+            if (t == 0) DIAG_STAMP(3 + p);
         }
-        __syncthreads();
     }
 }
 
-// Window load (global → shared) with periodic wrap: warps take rows, lanes take VEC-byte chunks.
+// ---- TMA bulk copies (cp.async.bulk, Hopper+/Blackwell) ----------------------------------------
+__device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra WAIT_%=;\n\t}" ::"r"(mbar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src), "r"(bytes)
+                 : "memory");
+}
+
+// Window load (global → shared) with periodic wrap.  TMA path: one bulk copy per row segment
+// (two when the row wraps), completion tracked by one mbarrier; fallback: vector loads.
 template <int VEC>
 __device__ __forceinline__ void load_window(uint8_t* win, const uint8_t* src, int H, int L, int P, int Wh, int Ww,
                                             int wy0, int wx0) {
@@ -410,14 +484,28 @@ __device__ __forceinline__ void load_window(uint8_t* win, const uint8_t* src, in
     }
 }
 
+__device__ __forceinline__ void load_window_tma(uint8_t* win, const uint8_t* src, int H, int L, int P, int Wh, int Ww,
+                                                int wy0, int wx0, uint32_t mbar) {
+    // caller: mbarrier initialised and expect_tx(Wh*Ww) armed by thread 0 before a __syncthreads
+    const uint32_t w0 = smem_addr(win);
+    for (int wr = threadIdx.x; wr < Wh; wr += blockDim.x) {
+        int gy = wy0 + wr;
+        gy = gy >= H ? gy - H : gy;
+        const uint8_t* srow = src + static_cast<size_t>(gy) * L;
+        const int n1 = (wx0 + Ww <= L) ? Ww : L - wx0;
+        bulk_g2s(w0 + wr * P, srow + wx0, static_cast<uint32_t>(n1), mbar);
+        if (n1 < Ww) bulk_g2s(w0 + wr * P + n1, srow, static_cast<uint32_t>(Ww - n1), mbar);
+    }
+}
+
 template <int VEC>
 __device__ __forceinline__ void store_block(uint8_t* dst, const uint8_t* win, int L, int P, int bh, int bw, int ry0,
-                                            int rx0) {
+                                            int rx0, int My, int Mx) {
     using V = typename std::conditional<VEC == 16, uint4, uint32_t>::type;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int cpr = bw / VEC;
     for (int y = warp; y < bh; y += nw) {
-        const V* srow = reinterpret_cast<const V*>(win + (kMargin + y) * P + kMarginX);
+        const V* srow = reinterpret_cast<const V*>(win + (My + y) * P + Mx);
         uint8_t* drow = dst + static_cast<size_t>(ry0 + y) * L + rx0;
         for (int c = lane; c < cpr; c += 32) {
             if (VEC == 16)
@@ -430,15 +518,16 @@ __device__ __forceinline__ void store_block(uint8_t* dst, const uint8_t* win, in
 
 template <int ARITY>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     const int r = blockIdx.z;
     if (a.run.status[r] != kStatusRunning) return;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
+    const int My = margin_rows(a.nmcs), Mx = margin_cols(a.nmcs);
     const int ry0 = a.row_split[blockIdx.y], ry1 = a.row_split[blockIdx.y + 1];
     const int rx0 = a.col_split[blockIdx.x], rx1 = a.col_split[blockIdx.x + 1];
     const int bh = ry1 - ry0, bw = rx1 - rx0;
-    const int Wh = bh + 2 * kMargin, Ww = bw + 2 * kMarginX;
+    const int Wh = bh + 2 * My, Ww = bw + 2 * Mx;
     const size_t N = static_cast<size_t>(H) * L;
     const uint8_t* src = a.src + r * N;
     uint8_t* dst = a.dst + r * N;
@@ -448,35 +537,66 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     int2* tblp = reinterpret_cast<int2*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15));
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(tblp + 32);
     __shared__ int sLast;
-    // 16-byte chunks when every window/block column boundary is 16-aligned in global memory
+    __shared__ __align__(8) uint64_t sMbar;
+    // 16-byte chunks / TMA rows when every window/block column boundary is 16-aligned in memory;
+    // TMA also needs the window to wrap at most once per axis.
     const bool v16 = (L & 15) == 0 && (rx0 & 15) == 0 && (bw & 15) == 0;
+    const bool tma = v16 && Wh <= H && Ww <= L;
+    DIAG_STAMP(0);
 
     if (a.step) {
         const uint32_t s32 = seed32(a.seeds[r]);
-        const int wy0 = ((ry0 - kMargin) % H + H) % H;
-        const int wx0 = ((rx0 - kMarginX) % L + L) % L;
+        const int wy0 = ((ry0 - My) % H + H) % H;
+        const int wx0 = ((rx0 - Mx) % L + L) % L;
+        const uint32_t mbar = smem_addr(&sMbar);
+#ifndef ESCG_DIAG_NO_LOAD
+        if (tma) {
+            if (tid == 0) {
+                mbar_init(mbar, 1);
+                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+                mbar_expect_tx_arrive(mbar, static_cast<uint32_t>(Wh * Ww));
+            }
+            __syncthreads();
+            load_window_tma(win, src, H, L, P, Wh, Ww, wy0, wx0, mbar);
+        } else if (v16) {
+            load_window<16>(win, src, H, L, P, Wh, Ww, wy0, wx0);
+        } else {
+            load_window<4>(win, src, H, L, P, Wh, Ww, wy0, wx0);
+        }
+#endif
         for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
         build_offset_table<ARITY>(tblp, P);
-        if (v16)
-            load_window<16>(win, src, H, L, P, Wh, Ww, wy0, wx0);
-        else
-            load_window<4>(win, src, H, L, P, Wh, Ww, wy0, wx0);
+        DIAG_STAMP(1);
+#ifndef ESCG_DIAG_NO_LOAD
+        if (tma) mbar_wait(mbar, 0);
+#endif
         __syncthreads();
+        DIAG_STAMP(2);
         const uint32_t win0 = smem_addr(win), tbl = smem_addr(tblp), sTa = smem_addr(sT);
         if (a.narrow)
-            block_phases<ARITY, true>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32, static_cast<uint64_t>(a.mcs));
+            block_phases<ARITY, true>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32, static_cast<uint64_t>(a.mcs));
-        if (v16)
-            store_block<16>(dst, win, L, P, bh, bw, ry0, rx0);
-        else
-            store_block<4>(dst, win, L, P, bh, bw, ry0, rx0);
+            block_phases<ARITY, false>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+#ifndef ESCG_DIAG_NO_LOAD
+        if (tma) {
+            // generic-proxy writes → async proxy, then one bulk store per block row
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            for (int y = tid; y < bh; y += nt)
+                bulk_s2g(dst + static_cast<size_t>(ry0 + y) * L + rx0, win0 + (My + y) * P + Mx, static_cast<uint32_t>(bw));
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        } else if (v16) {
+            store_block<16>(dst, win, L, P, bh, bw, ry0, rx0, My, Mx);
+        } else {
+            store_block<4>(dst, win, L, P, bh, bw, ry0, rx0, My, Mx);
+        }
+#endif
     }
     if (a.count) {
         for (int v = tid; v < S1; v += nt) sCnt[v] = 0;
         __syncthreads();
         if (a.step)
-            block_count(win + kMargin * P + kMarginX, bh, bw, P, S1, sCnt);
+            block_count(win + My * P + Mx, bh, bw, P, S1, sCnt);
         else
             block_count(src + static_cast<size_t>(ry0) * L + rx0, bh, bw, L, S1, sCnt);
         __syncthreads();
@@ -493,11 +613,15 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
             uint64_t c64[kMaxSpecies + 1];
             for (int v = 0; v < S1; ++v) c64[v] = atomicExch(&a.acc[r * S1 + v], 0ull);
             a.ticket[r] = 0u;
-            record_decide(c64, S1, a.mcs + a.step, r, a.run);
+            if (a.run.cur) a.run.cur[r] = a.step ? a.dst_index : 1 - a.dst_index;
+            record_decide(c64, S1, a.mcs + (a.step ? a.nmcs : 0), r, a.run);
         }
     }
+    DIAG_STAMP(8);
+    // bulk stores must finish reading shared memory before the CTA exits
+    if (a.step && tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    DIAG_STAMP(9);
 }
-
 
 // ---------------------------------------------------------------------------------------------
 // Helpers
@@ -597,9 +721,26 @@ int grid_for(int64_t n, int threads) {
 }  // namespace
 
 int tile_smem_bytes(int H, int L, int S, int* pitch) {
-    const int P = align16(L + kTileC0 + 1);
+    // pitch ≡ 0 (mod 128) keeps a tile's footprint column in one bank group (conflict-light
+    // accesses); fall back to 16-byte alignment when the padded lattice would not fit.
+    int P = (L + kTileC0 + 1 + 127) & ~127;
+    if (tile_layout(H, L, S, P).total > max_smem_optin(0)) P = align16(L + kTileC0 + 1);
     if (pitch) *pitch = P;
     return tile_layout(H, L, S, P).total;
+}
+
+// Diagnostic: copy the block kernel's section stamps (ESCG_DIAG_TIMING builds; else returns 0).
+extern "C" __attribute__((visibility("default"))) int escg_diag_timing(unsigned long long* out, int n) {
+#ifdef ESCG_DIAG_TIMING
+    return cudaMemcpyFromSymbol(out, g_diag_t, sizeof(unsigned long long) * (n < 4096 * 16 ? n : 4096 * 16)) ==
+                   cudaSuccess
+               ? n
+               : -1;
+#else
+    (void)out;
+    (void)n;
+    return 0;
+#endif
 }
 
 int max_smem_optin(int device) {

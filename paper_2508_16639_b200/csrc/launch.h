@@ -9,8 +9,11 @@ namespace escgd {
 
 // Margin of the overlapped-tile (block) kernel: a tile footprint reaches 3 cells past the tile
 // origin, so validity shrinks by 3 cells per phase and 4 phases need 12 cells.
-constexpr int kMargin = 12;   // rows
-constexpr int kMarginX = 16;  // columns: 12 + 4 so window column 0 stays 8-aligned (NARROW pairs)
+// With k MCS per launch (temporal blocking) the margin is 12k rows and 12k+4 columns rounded up to
+// a multiple of 16 (window column 0 stays 16-aligned: TMA rows and NARROW tile pairs).
+constexpr int kMaxBlockMcs = 4;
+__host__ __device__ constexpr int margin_rows(int k) { return 12 * k; }
+__host__ __device__ constexpr int margin_cols(int k) { return (12 * k + 4 + 15) & ~15; }
 // Tile-kernel window: rows -2..H, cols -2..L (ghost frame of the periodic wrap), origin (2, 4).
 constexpr int kTileR0 = 2;
 constexpr int kTileC0 = 4;
@@ -30,6 +33,7 @@ struct RunArgs {
     int64_t* trace_steps;     // [rep][cap] or nullptr
     uint64_t* trace_counts;   // [rep][cap][S+1] or nullptr
     int64_t trace_cap;
+    int32_t* cur;             // block path: buffer (0/1) holding the lattice at the last record
     int64_t mcs_limit;
     int64_t interval;
     uint32_t stop_flags;
@@ -60,8 +64,10 @@ struct BlockArgs {
     int nby, nbx;
     const int* row_split;  // nby+1 row boundaries (multiples of 4)
     const int* col_split;  // nbx+1
-    int64_t mcs;           // MCS executed by this launch
-    int step;              // 1: execute MCS `mcs` (src → dst); 0: count src only
+    int64_t mcs;           // first MCS executed by this launch
+    int nmcs;              // MCS per launch (temporal blocking, margins margin_rows/cols(nmcs))
+    int dst_index;         // buffer index of dst (recorded with the density record)
+    int step;              // 1: execute MCS [mcs, mcs+nmcs) (src → dst); 0: count src only
     int count;             // 1: record densities of the result (at mcs+step)
     unsigned long long* acc;  // [rep][S+1] cross-CTA accumulators (zero between records)
     unsigned int* ticket;     // [rep]
