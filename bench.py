@@ -1,0 +1,331 @@
+"""bench.py — site-update attempts/s of the ESCG Monte Carlo step path at L=3200 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[2], the headline): RPS (C(3,{1})) on a 3200x3200 periodic von-Neumann
+lattice, M=1e-4, empty_prob 0.1, EngineMode::MaxStep record cadence (align(1e8, N)/N = 9 MCS per density
+record, on-device stasis check).  One step = 900 MCS (100 records).  Inputs are resident in HBM when the
+timed region starts (`value`); L2 (126 MB) is flushed between steps since the lattice fits in it.
+`e2e` runs the same step through the C ABI (escg_simulate: simulate() with a host int32 lattice from
+pinned memory in, final lattice + density trace out).  N>1: one independent lattice per GPU
+(replicas, seed + rank), no data-path collective (weak scaling).
+
+--impl reference times the unmodified reference engine (oracle/_ref, run_max_step with ThreadPool(nproc),
+EngineMode::MaxStep) on the host cores on a bounded sample of the same workload; rank 0 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L = 3200
+M = 1e-4
+P0 = 0.1
+NUM_RANDOMS = 100000000
+MCS_PER_STEP = 900
+METRIC = "site-update attempts/sec and MCS/sec at L=3200 (1/2/4/8 B200) vs CPU ref"
+UNIT = "attempts/s"
+# BASELINE.md / PAPER.md:1366: CUDA-MS (maxStep) L=3200 on RTX A2000, 4173.50 s for 1e5 MCS
+PUBLISHED_ATTEMPTS_PER_S = 3200 * 3200 * 1e5 / 4173.50
+
+
+def workload_config(extra=None):
+    cfg = {"workload": "RPS C(3,{1}) L=3200 M=1e-4 p0=0.1 VN4 periodic, MaxStep record cadence (9 MCS), "
+                       "%d MCS per step" % MCS_PER_STEP,
+           "L": L, "species": 3, "mobility": M, "empty_prob": P0, "num_randoms": NUM_RANDOMS,
+           "mcs_per_step": MCS_PER_STEP, "l2": "flushed between timed steps (256 MiB device write)",
+           "vs_baseline_ref": "PAPER.md:1366 CUDA-MS L=3200 RTX A2000: 4173.50 s / 1e5 MCS = %.3g attempts/s"
+                              % PUBLISHED_ATTEMPTS_PER_S}
+    if extra:
+        cfg.update(extra)
+    return cfg
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU reference (oracle/_ref = unmodified reference engine)
+# ---------------------------------------------------------------------------------------------
+
+def reference_sample(mcs, mode=2, workers=None, seed=1):
+    """simulate(params, C(3,{1}), mode) on the host; returns (attempts/s, wall s of the timed window,
+    workers).  Window: first on_record → return, so init and burn-in are excluded."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    from pyoracle import Reference
+
+    r = Reference()
+    workers = workers or os.cpu_count()
+    dom = r.circulant(3, [1])
+    num_randoms = L * L * 5  # 5 MCS per batch (≈ the paper's optimum), double-buffered
+    res = r.simulate(L, L, dom, M, P0, mcs, seed, mode=mode, workers=workers if mode else 1,
+                     num_randoms=num_randoms, cap=mcs + 2, want_cells=False)
+    elapsed = res["elapsed_s"]
+    return L * L * mcs / elapsed, elapsed, (workers if mode else 1)
+
+
+def cpu_baseline():
+    v, el, w = reference_sample(mcs=20, mode=2)
+    return {"value": v, "unit": UNIT, "cores": w, "kind": "reference",
+            "sample": "reference run_max_step (ThreadPool(%d)), RPS L=3200 M=1e-4 p0=0.1, 20 MCS window "
+                      "from the first density record (%.1f s wall)" % (w, el)}
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    try:
+        from pyoracle import Reference  # noqa: F401
+    except Exception:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    times, vals = [], []
+    for i in range(args.warmup + args.steps):
+        v, el, w = reference_sample(mcs=10, mode=2, seed=1 + i)
+        if i >= args.warmup:
+            vals.append(v)
+            times.append(el)
+    value = L * L * 10 * len(times) / sum(times)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": value / PUBLISHED_ATTEMPTS_PER_S, "dtype": "int32", "data": "synthetic",
+            "impl": "reference", "mcs_per_s": value / (L * L),
+            "config": workload_config({"step": "10 MCS of run_max_step (numRandoms = 5N: two double-buffered "
+                                               "batches) per step, window from the first density record"}),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                             "sample": "10 MCS per step x %d steps, ThreadPool(%d)" % (args.steps, os.cpu_count())},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------------------------
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, device, enabled=True):
+        self.device = device
+        self.enabled = enabled
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", "bench_clocks_%d.csv" % os.getpid())
+
+    def __enter__(self):
+        if not self.enabled:
+            return self
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=10)
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) >= 9:
+                try:
+                    rows.append((float(p[1]), float(p[2]), float(p[3]), p[5:9]))
+                except ValueError:
+                    pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        load = [r for r in rows if r[2] > 150.0] or rows
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in load for i, v in enumerate(r[3]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in load), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(load)}
+
+
+def peak_hbm():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(path))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        d = json.load(open(path))
+        return d.get("dram_bytes_per_launch"), d.get("mcs_per_launch")
+    except Exception:
+        return None, None
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2508_16639_b200 as e
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    seed = 20240601 + rank
+    model = e.make_circulant(3, [1])
+    params = e.SimParams(length=L, height=L, species=3, mobility=M, empty_prob=P0, num_randoms=NUM_RANDOMS,
+                         max_step=True, seed=seed, mcs_limit=10 ** 12)
+    N = L * L
+    interval = e.align_num_randoms(NUM_RANDOMS, N) // N
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+
+    eng = e.DeviceEngine(params, model, 1, device=local)
+    eng.init_lattice()
+    desc = eng.describe()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def step():
+        m0 = eng.mcs()
+        st = eng.run(m0 + MCS_PER_STEP, interval=interval, record_trace=False)
+        ms, launches = eng.last_timing()
+        return ms, launches, int(st[0])
+
+    for _ in range(args.warmup):
+        step()
+    times, launches = [], 0
+    with ClockSampler(local, enabled=not os.environ.get("ESCG_BENCH_NO_CLOCKS")) as clk:
+        barrier()
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            if not os.environ.get("ESCG_BENCH_NO_FLUSH"):
+                flush.fill_(1)  # untimed L2 flush (the lattice fits in L2)
+            torch.cuda.synchronize()
+            ms, n, st = step()
+            if os.environ.get("ESCG_BENCH_VERBOSE"):
+                print("step %.2f ms launches %d" % (ms, n), file=sys.stderr)
+            times.append(ms)
+            launches += n
+        torch.cuda.synchronize()
+        barrier()
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    attempts = N * MCS_PER_STEP * args.steps * world
+    value = attempts / (total_ms / 1e3)
+
+    # e2e through the C ABI (escg_simulate = simulate() mirror): host int32 lattice in (pinned),
+    # device init skipped (resume), run 900 MCS with records, final lattice + density trace out (pinned).
+    import ctypes as C
+
+    from paper_2508_16639_b200 import _lib
+
+    lat_in = torch.empty(N, dtype=torch.int32).pin_memory().numpy()
+    lat_out = torch.empty(N, dtype=torch.int32).pin_memory().numpy()
+    lat_in[:] = eng.get_lattice(0)
+    mcs0 = eng.mcs()
+    eng.close()
+    cap = MCS_PER_STEP // interval + 2
+    steps_buf = torch.empty(cap, dtype=torch.int64).pin_memory().numpy()
+    counts_buf = torch.empty(cap * 4, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    dom = np.ascontiguousarray(model.entries, np.float64)
+    out_mcs, n_rec, status = C.c_int64(0), C.c_int64(0), C.c_int32(0)
+    lib = _lib.lib()
+    e2e_times = []
+    cur = mcs0
+    for i in range(args.warmup + args.steps):
+        p = e.SimParams(**{**params.__dict__, "mcs_limit": cur + MCS_PER_STEP}).to_c(seed)
+        barrier()
+        t0 = time.perf_counter()
+        _lib.check(lib.escg_simulate(C.byref(p), dom, 3, 0, int(e.EngineMode.MaxStep), local, _lib.ptr(lat_in), cur, 0, 0,
+                                     _lib.ptr(lat_out), C.byref(out_mcs), _lib.ptr(steps_buf), _lib.ptr(counts_buf), cap,
+                                     C.byref(n_rec), C.byref(status)))
+        t1 = time.perf_counter()
+        if i >= args.warmup:
+            e2e_times.append(t1 - t0)
+        lat_in, lat_out = lat_out, lat_in
+        cur = out_mcs.value
+    e2e_s = sum(e2e_times)
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = N * MCS_PER_STEP * args.steps * world / e2e_s
+    n_records = MCS_PER_STEP // interval + 1
+
+    if rank == 0:
+        peak, peak_src = peak_hbm()
+        per_gpu = value / world
+        traffic, tr_mcs = ncu_traffic()
+        roof = {"bound": "hbm", "achieved": per_gpu * 2 / 1e9, "peak": peak, "unit": "GB/s",
+                "frac": per_gpu * 2 / 1e9 / peak, "peak_source": peak_src,
+                "traffic": traffic, "kernel": "block_kernel (overlapped-tile CRS, %d MCS/launch)" % desc.get("kmcs", 1),
+                "algorithmic_bytes": "2 B per site-update attempt (1 B read + 1 B write of the uint8 lattice per "
+                                     "site per MCS); achieved = attempts/s x 2 B over the device-timed region",
+                "avg_launch_us": total_ms / max(launches, 1) * 1e3,
+                "traffic_per_launch_mcs": tr_mcs}
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": value / PUBLISHED_ATTEMPTS_PER_S, "dtype": "u8",
+                "data": "synthetic (Philox-initialised random lattice, empty_prob 0.1)",
+                "mcs_per_s": value / N / world,
+                "config": workload_config({"parallelism": "replicas x%d (one lattice per GPU)" % world,
+                                           "kernel": desc}),
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * N,
+                        "d2h_bytes_per_step": 4 * N + n_records * (8 + 4 * 8) + 8,
+                        "path": "escg_simulate C ABI (simulate() mirror), pinned host int32 lattice in/out"},
+                "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = cpu_baseline()
+            except Exception as ex:  # reported, never fatal
+                line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                                        "sample": "unavailable: %s" % ex}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

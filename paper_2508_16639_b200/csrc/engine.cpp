@@ -184,7 +184,8 @@ struct escg_dev {
     int narrow = 0;  // draw format
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     cudaStream_t stream = nullptr;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_poll = nullptr;
+    int32_t* h_status = nullptr;  // pinned, status polling of the block path
     Thresholds th;
     uint32_t x_empty = 0;
     std::vector<uint64_t> seeds;
@@ -207,6 +208,8 @@ struct escg_dev {
     int64_t last_launches = 0;
 
     ~escg_dev() {
+        if (h_status) cudaFreeHost(h_status);
+        if (ev_poll) cudaEventDestroy(ev_poll);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         if (stream) cudaStreamDestroy(stream);
@@ -442,10 +445,8 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         ++launches;
         // Poll the device status every few chunks so a stasis/stop does not leave thousands of
         // no-op launches queued; the poll lags one chunk behind the enqueue front.
-        int32_t* hstat = nullptr;
-        CK(cudaMallocHost(&hstat, sizeof(int32_t) * h->nrep));
-        cudaEvent_t polled = nullptr;
-        CK(cudaEventCreateWithFlags(&polled, cudaEventDisableTiming));
+        int32_t* hstat = h->h_status;
+        cudaEvent_t polled = h->ev_poll;
         bool poll_pending = false;
         int64_t t = t0, since_poll = 0;
         const int64_t kChunk = 512;
@@ -467,8 +468,6 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
                 poll_pending = true;
             }
         }
-        cudaEventDestroy(polled);
-        cudaFreeHost(hstat);
     }
     timed_end(h, launches);
     CK(cudaGetLastError());
@@ -609,6 +608,8 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&h->ev0));
         CK(cudaEventCreate(&h->ev1));
+        CK(cudaEventCreateWithFlags(&h->ev_poll, cudaEventDisableTiming));
+        CK(cudaMallocHost(&h->h_status, sizeof(int32_t) * n_replicas));
         h->lat[0].alloc(static_cast<size_t>(h->N) * n_replicas);
         if (choice == ESCG_KERNEL_TILE) {
             h->P = tpitch;
@@ -861,6 +862,13 @@ int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t*
     });
 }
 
+int escg_dev_block_mcs(escg_dev* h, int32_t* kmcs) {
+    return guarded([&] {
+        if (!h || !kmcs) config_error("null argument");
+        *kmcs = h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1;
+    });
+}
+
 int escg_dev_draw_format(escg_dev* h, int32_t* narrow) {
     return guarded([&] {
         if (!h || !narrow) config_error("null argument");
@@ -892,7 +900,18 @@ int escg_simulate(const escg_params* p, const double* dominance, int32_t species
         };
         thread_local Cache cache;
         std::vector<double> dom(dominance, dominance + static_cast<size_t>(species) * species);
-        escg_params key = *p;
+        // only the fields that shape the engine (geometry, model, rates, seed) key the cache;
+        // mcs_limit / num_randoms / print_frequency / flags vary per call
+        escg_params key{};
+        key.length = p->length;
+        key.height = p->height;
+        key.neighbourhood = p->neighbourhood;
+        key.mobility = p->mobility;
+        key.species = p->species;
+        key.flux = p->flux;
+        key.empty_prob = p->empty_prob;
+        key.has_seed = p->has_seed;
+        key.seed = p->seed;
         const bool same = cache.h && cache.kind == kind && cache.device == device && cache.dom == dom &&
                           std::memcmp(&cache.p, &key, sizeof(escg_params)) == 0;
         if (!same) {
@@ -908,6 +927,7 @@ int escg_simulate(const escg_params* p, const double* dominance, int32_t species
             cache.device = device;
         }
         escg_dev* h = cache.h;
+        h->p = *p;
         int rc;
         if (resume_cells)
             rc = escg_dev_set_lattice(h, 0, resume_cells, resume_mcs);
