@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -571,7 +572,9 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
         h->N = static_cast<int64_t>(h->H) * h->L;
         h->device = device;
         h->nrep = n_replicas;
-        const uint64_t base_seed = p->has_seed ? p->seed : 0x5EEDull;
+        // no seed: non-reproducible like the reference (std::random_device, engine.cpp:210)
+        const uint64_t base_seed =
+            p->has_seed ? p->seed : ((static_cast<uint64_t>(std::random_device{}()) << 32) | std::random_device{}());
         h->seeds.resize(n_replicas);
         for (int r = 0; r < n_replicas; ++r) h->seeds[r] = replica_seeds ? replica_seeds[r] : base_seed + r;
         h->th = compute_thresholds(p->mobility, h->N, dominance, species);
@@ -883,6 +886,12 @@ int escg_simulate(const escg_params* p, const double* dominance, int32_t species
     return guarded([&] {
         if (!p) config_error("null params");
         validate_params(*p);
+        escg_params pp = *p;  // a missing seed is drawn per call (engine.cpp:210 random_device)
+        if (!pp.has_seed) {
+            pp.has_seed = 1;
+            pp.seed = (static_cast<uint64_t>(std::random_device{}()) << 32) | std::random_device{}();
+        }
+        p = &pp;
         const int64_t N = static_cast<int64_t>(p->length) * p->height;
         int64_t interval = 1;
         if (mode == ESCG_MODE_MAX_STEP) interval = align_num_randoms_or_throw(p->num_randoms, N) / N;

@@ -248,3 +248,18 @@ def test_simulate_one_call_matches_handle_path(escg, oracle):
                          hooks=escg.RunHooks(on_record=lambda st: seen.append(st.current_mcs) or True))
     assert seen == list(range(41))
     assert np.array_equal(res2.state.lattice.cells, want)
+
+
+def test_device_replica_runner_matches_single_engine(escg):
+    """dist.device_replica_runner (the per-rank body of a sharded ensemble) == per-seed engines."""
+    from paper_2508_16639_b200.dist import device_replica_runner, run_sharded
+
+    p = params(escg, 32, 32, 3, 1e-3, 0.1, 4, True, mcs=30)
+    model = escg.make_circulant(3, [1])
+    res = run_sharded([5, 6, 7], device_replica_runner(p, model))
+    for s, (m, st, counts) in zip([5, 6, 7], res):
+        q = params(escg, 32, 32, 3, 1e-3, 0.1, 4, True, seed=s, mcs=30)
+        with escg.DeviceEngine(q, model, kernel="block") as eng:
+            eng.init_lattice()
+            eng.run(30, interval=1, record_trace=False)
+            assert eng.replica_result(0)[2].tolist() == counts and m == 30
