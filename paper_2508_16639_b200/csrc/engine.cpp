@@ -226,7 +226,7 @@ size_t block_smem(int bh, int bw, int S1, int k, int* pitch) {
     const int P = ((bw + 2 * escgd::margin_cols(k)) + 127) & ~127;
     if (pitch) *pitch = P;
     return static_cast<size_t>((((bh + 2 * escgd::margin_rows(k)) * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) +
-                               32 * 8 + (escgd::kMaxSpecies + 1) * 4 + 64);
+                               32 * 8 + (escgd::kMaxSpecies + 1) * 4 + 4 * P + 64);  // + scratch box
 }
 
 // Block-kernel decomposition: row splits at multiples of 4, column splits at multiples of 16 (8, 4)

@@ -340,23 +340,31 @@ __device__ __forceinline__ int wrap_down(int v, int n, bool big) {
     return v >= n ? v - n : v;
 }
 
+// Per-launch constants of the phase loop (by value: keeps the kernel-parameter block out of local
+// memory).
+struct BlockGeom {
+    int P, H, L, nmcs;
+    int64_t mcs;
+    uint32_t scratch;  // smem address of a dummy 4-row box (edge items with one invalid tile)
+};
+
 template <int ARITY, bool NARROW>
-__device__ __forceinline__ void block_phases(const BlockArgs& a, uint32_t win0, uint32_t tbl, uint32_t sT, int S1,
-                                             int Wh, int Ww, int wy0, int wx0, uint32_t s32) {
-    const int tid = threadIdx.x, nt = blockDim.x, P = a.P;
-    const int Ty = a.H >> 1, Tx = a.L >> 1, TQ = a.L >> 3;
+__device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs rule, uint32_t win0, uint32_t tbl,
+                                             uint32_t sT, int S1, int Wh, int Ww, int wy0, int wx0, uint32_t s32) {
+    const int tid = threadIdx.x, nt = blockDim.x, P = g.P;
+    const int Ty = g.H >> 1, Tx = g.L >> 1, TQ = g.L >> 3;
     const int jb = wy0 >> 1, ib = wx0 >> 1;  // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
-    const int ex = margin_cols(a.nmcs) - margin_rows(a.nmcs);  // extra loaded columns
-    const bool big = Wh > a.H || Ww > a.L;  // window wraps more than once: use a true modulo
+    const int ex = margin_cols(g.nmcs) - margin_rows(g.nmcs);  // extra loaded columns
+    const bool big = Wh > g.H || Ww > g.L;  // window wraps more than once: use a true modulo
 #pragma unroll 1
-    for (int t = 0; t < a.nmcs; ++t) {
-        const uint64_t mcs = static_cast<uint64_t>(a.mcs + t);
+    for (int t = 0; t < g.nmcs; ++t) {
+        const uint64_t mcs = static_cast<uint64_t>(g.mcs + t);
         const Round rp = round_params(s32, mcs);
 #pragma unroll 1
         for (int p = 0; p < 4; ++p) {
             const int q = 4 * t + p;  // global phase of this launch: validity shrinks 3 cells per phase
             const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-            const PhaseCtx C = phase_ctx<ARITY>(a.rule, NARROW, tbl, sT, S1, mcs, p, s32);
+            const PhaseCtx C = phase_ctx<ARITY>(rule, NARROW, tbl, sT, S1, mcs, p, s32);
             const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
             // footprint rows [2j-oy-1, 2j-oy+2] within [3q, Wh-3q); cols within [ex+3q, Ww-ex-3q)
             const int lo = 3 * q, hiR = Wh - 3 * q, loC = ex + 3 * q, hiC = Ww - ex - 3 * q;
@@ -365,7 +373,8 @@ __device__ __forceinline__ void block_phases(const BlockArgs& a, uint32_t win0, 
             const int j0 = jmin + ((jmin ^ cy) & 1);
             const int nj = jmax >= j0 ? ((jmax - j0) >> 1) + 1 : 0;
             // items: pairs of same-colour tiles (i, i+2).  NARROW pairs are the global draw pairs
-            // (window column 0 is 8-aligned); WIDE pairs are local.  Edge items may hold one tile.
+            // (window column 0 is 8-aligned); WIDE pairs are local.  A tile outside the valid region
+            // runs on the scratch box (same instruction stream for every lane, results discarded).
             const int i0 = imin + ((imin ^ cx) & 1);  // first valid tile column of this colour
             int u0, nu;
             if (NARROW) {
@@ -382,42 +391,54 @@ __device__ __forceinline__ void block_phases(const BlockArgs& a, uint32_t win0, 
                 const int q0 = udiv_small(tid, nu), qn = udiv_small(nt, nu);
                 int aa = q0, bb = tid - q0 * nu;
                 const int da = qn, db = nt - qn * nu;
-                for (int k = tid; k < cnt; k += nt) {
-                    const int j = j0 + 2 * aa;
+                // item geometry + draw of item (aa, bb); the draw of the next item is computed
+                // before the current item's attempts (software pipelining of the Philox latency)
+                auto geom = [&](int a_, int b_, uint32_t& bA, uint32_t& bB, uint32_t& tA, uint32_t& tB, uint4& w) {
+                    const int j = j0 + 2 * a_;
                     const int ty = wrap_down(jb + j, Ty, big);
                     const uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
                     const uint32_t trow = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx);
+                    int ia;
                     if (NARROW) {
-                        const int u = u0 + bb;
+                        const int u = u0 + b_;
                         const int qq = wrap_down((ib >> 2) + u, TQ, big);
-                        const uint4 w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(TQ) + qq, C.c1, c2, s32);
-                        const int ia = cx + 4 * u;
-                        const uint32_t t0 = trow + 4 * qq + cx;
-                        const bool okA = ia >= imin && ia <= imax, okB = ia + 2 >= imin && ia + 2 <= imax;
-                        if (okA & okB) {
-                            pair_narrow<ARITY>(w, rowbase + 2 * ia, t0, rowbase + 2 * ia + 4, t0 + 2, C);
-                        } else {
-                            if (okA) tile_narrow<ARITY>(w.x, w.y, rowbase + 2 * ia, t0, C);
-                            if (okB) tile_narrow<ARITY>(w.z, w.w, rowbase + 2 * ia + 4, t0 + 2, C);
-                        }
+                        w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(TQ) + qq, C.c1, c2, s32);
+                        ia = cx + 4 * u;
+                        tA = trow + 4 * qq + cx;
+                        tB = tA + 2;
                     } else {
-                        const int ia = i0 + 4 * bb;
-                        const uint32_t tA = trow + wrap_down(ib + ia, Tx, big);
-                        const uint4 wA = philox(tA, C.c1, c2, s32);
-                        if (ia + 2 <= imax) {
-                            const uint32_t tB = trow + wrap_down(ib + ia + 2, Tx, big);
-                            pair_wide<ARITY>(wA, rowbase + 2 * ia, tA, philox(tB, C.c1, c2, s32), rowbase + 2 * ia + 4,
-                                             tB, C);
-                        } else {
-                            tile_wide<ARITY>(wA, rowbase + 2 * ia, tA, C);
-                        }
+                        ia = i0 + 4 * b_;
+                        tA = trow + wrap_down(ib + ia, Tx, big);
+                        tB = trow + wrap_down(ib + ia + 2, Tx, big);
+                        w = philox(tA, C.c1, c2, s32);
                     }
+                    const bool okA = ia >= imin && ia <= imax, okB = ia + 2 >= imin && ia + 2 <= imax;
+                    bA = okA ? rowbase + 2 * ia : g.scratch;
+                    bB = okB ? rowbase + 2 * ia + 4 : g.scratch + 8;
+                };
+                uint32_t bA, bB, tA, tB;
+                uint4 w;
+                geom(aa, bb, bA, bB, tA, tB, w);
+                for (int k = tid; k < cnt; k += nt) {
                     bb += db;
                     aa += da;
                     if (bb >= nu) {
                         bb -= nu;
                         ++aa;
                     }
+                    uint32_t nA = 0, nB = 0, ntA = 0, ntB = 0;
+                    uint4 nw = make_uint4(0, 0, 0, 0);
+                    if (k + nt < cnt) geom(aa, bb, nA, nB, ntA, ntB, nw);
+                    if (NARROW) {
+                        pair_narrow<ARITY>(w, bA, tA, bB, tB, C);
+                    } else {
+                        pair_wide<ARITY>(w, bA, tA, philox(tB, C.c1, c2, s32), bB, tB, C);
+                    }
+                    bA = nA;
+                    bB = nB;
+                    tA = ntA;
+                    tB = ntB;
+                    w = nw;
                 }
             }
 #ifndef ESCG_DIAG_NO_PHASE_SYNC
@@ -536,6 +557,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
     int2* tblp = reinterpret_cast<int2*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15));
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(tblp + 32);
+    uint8_t* sScratch = reinterpret_cast<uint8_t*>(sCnt + kMaxSpecies + 1);  // 4 * P bytes (dummy box)
     __shared__ int sLast;
     __shared__ __align__(8) uint64_t sMbar;
     // 16-byte chunks / TMA rows when every window/block column boundary is 16-aligned in memory;
@@ -566,6 +588,8 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
 #endif
         for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
         build_offset_table<ARITY>(tblp, P);
+        // the scratch box must hold valid species codes: dummy attempts index the threshold table
+        for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
         DIAG_STAMP(1);
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) mbar_wait(mbar, 0);
@@ -573,10 +597,17 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         __syncthreads();
         DIAG_STAMP(2);
         const uint32_t win0 = smem_addr(win), tbl = smem_addr(tblp), sTa = smem_addr(sT);
+        BlockGeom g;
+        g.P = P;
+        g.H = H;
+        g.L = L;
+        g.nmcs = a.nmcs;
+        g.mcs = a.mcs;
+        g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, true>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false>(a, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, false>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) {
             // generic-proxy writes → async proxy, then one bulk store per block row
