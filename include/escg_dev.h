@@ -150,8 +150,9 @@ ESCG_API int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas,
  * draw per tile pair) — DESIGN.md §RNG; the oracle needs it to replay the schedule. */
 ESCG_API int escg_dev_draw_format(escg_dev* h, int32_t* narrow);
 
-/* Block kernel: MCS per launch (temporal blocking; 1 for the tile kernel). */
-ESCG_API int escg_dev_block_mcs(escg_dev* h, int32_t* kmcs);
+/* Block kernel mode: MCS per chunk (temporal blocking; 1 for the tile kernel) and whether a run
+ * executes as one persistent cooperative launch (1) or one launch per chunk (0). */
+ESCG_API int escg_dev_block_mode(escg_dev* h, int32_t* kmcs, int32_t* persistent);
 
 /* One-call mirror of escg::simulate(params, model, mode, …) (engine.cpp:194-240) for a single
  * lattice: initialise on device (or resume from resume_cells at resume_mcs), run to completion

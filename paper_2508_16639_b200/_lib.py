@@ -45,7 +45,7 @@ EXPORTS = [
     "escg_align_num_randoms", "escg_dev_create", "escg_dev_destroy", "escg_dev_init_lattice", "escg_dev_set_lattice",
     "escg_dev_get_lattice", "escg_dev_counts", "escg_dev_advance", "escg_dev_run", "escg_dev_read_trace",
     "escg_dev_replica_result", "escg_dev_replay", "escg_dev_last_timing", "escg_dev_describe",
-    "escg_dev_draw_format", "escg_dev_block_mcs", "escg_simulate",
+    "escg_dev_draw_format", "escg_dev_block_mode", "escg_simulate",
 ]
 
 _lib = None
@@ -93,7 +93,7 @@ def lib():
     L.escg_dev_describe.argtypes = [_H, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                     C.POINTER(C.c_int32)]
     L.escg_dev_draw_format.argtypes = [_H, C.POINTER(C.c_int32)]
-    L.escg_dev_block_mcs.argtypes = [_H, C.POINTER(C.c_int32)]
+    L.escg_dev_block_mode.argtypes = [_H, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
     L.escg_simulate.argtypes = [_P, _f64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
                                 C.c_uint32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
                                 C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]

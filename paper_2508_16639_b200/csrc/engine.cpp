@@ -184,6 +184,8 @@ struct escg_dev {
     int nby = 1, nbx = 1;
     int narrow = 0;  // draw format
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
+    bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
+    int bh_max = 0, bw_max = 0;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_poll = nullptr;
     int32_t* h_status = nullptr;  // pinned, status polling of the block path
@@ -202,6 +204,7 @@ struct escg_dev {
     DevBuf<unsigned int> d_ticket;
     DevBuf<int> d_rows, d_cols, d_bad;
     DevBuf<int32_t> d_cur;
+    DevBuf<unsigned long long> d_acc3;
     DevBuf<int32_t> d_i32;
     int64_t trace_cap = 0;
     bool traced = false;
@@ -233,6 +236,10 @@ size_t block_smem(int bh, int bw, int S1, int k, int* pitch) {
 // when L allows (TMA rows, NARROW pairs), and k MCS per launch (temporal blocking).  Model per MCS:
 // waves x (mean valid area over the 4k phases + launch/load overhead / k), in cell units.
 void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
+    // CTAs resident per SM at h->threads threads and <= 64 registers/thread (1024 → 1, 512 → 2)
+    const int cta_per_sm = h->threads <= 512 ? 2 : 1;
+    sms *= cta_per_sm;
+    smem_cap = std::min(smem_cap, (228 * 1024) / cta_per_sm - 1024);
     const int cu = (h->L % 16 == 0) ? 16 : ((h->L % 8 == 0) ? 8 : 4);
     const int uy = h->H / 4, ux = h->L / cu;
     double best = 1e300;
@@ -266,6 +273,8 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
     h->smem = static_cast<int>(block_smem(bh, bw, h->S1, bk, &h->P));
+    h->bh_max = bh;
+    h->bw_max = bw;
     h->d_rows.alloc(rows.size());
     h->d_cols.alloc(cols.size());
     CK(cudaMemcpy(h->d_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
@@ -367,6 +376,30 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     return launches;
 }
 
+escgd::PersistArgs persist_args(escg_dev* h, const escgd::RunArgs& run) {
+    escgd::PersistArgs pa{};
+    escgd::BlockArgs& a = pa.b;
+    a.seeds = h->d_seeds.p;
+    a.rule = rule_args(h);
+    a.run = run;
+    a.H = h->H;
+    a.L = h->L;
+    a.S = h->S;
+    a.P = h->P;
+    a.arity = h->arity;
+    a.narrow = h->narrow;
+    a.nby = h->nby;
+    a.nbx = h->nbx;
+    a.row_split = h->d_rows.p;
+    a.col_split = h->d_cols.p;
+    a.smem_bytes = h->smem;
+    pa.buf[0] = h->lat[0].p;
+    pa.buf[1] = h->lat[1].p;
+    pa.kmcs = h->kmcs;
+    pa.acc3 = h->d_acc3.p;
+    return pa;
+}
+
 void ensure_trace(escg_dev* h, int64_t records) {
     const int64_t cap = std::max<int64_t>(records, 1);
     const double bytes = static_cast<double>(cap) * h->nrep * (h->S1 * 8 + 8);
@@ -411,6 +444,14 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.record = 1;
         a.smem_bytes = h->smem;
         CK(escgd::launch_tile(a, h->nrep, h->threads, h->stream));
+        launches = 1;
+    } else if (h->persist) {
+        CK(cudaMemsetAsync(h->d_acc3.p, 0, sizeof(unsigned long long) * 3 * h->S1 * h->nrep, h->stream));
+        escgd::PersistArgs pa = persist_args(h, run);
+        pa.mcs0 = h->mcs[0];
+        pa.mcs_end = limit;
+        pa.record = 1;
+        CK(escgd::launch_block_persistent(pa, h->nrep, h->threads, h->stream));
         launches = 1;
     } else {
         CK(cudaMemsetAsync(h->d_acc.p, 0, sizeof(unsigned long long) * h->S1 * h->nrep, h->stream));
@@ -620,11 +661,27 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
             h->threads = 512;
         } else {
             h->lat[1].alloc(static_cast<size_t>(h->N) * n_replicas);
+            // lattices far beyond one CTA per SM stream through many waves: two 512-thread CTAs per
+            // SM overlap one CTA's load/barrier phases with the other's attempts (measured, L=16384)
+            h->threads = h->N >= (int64_t{64} << 20) ? 512 : 1024;
+            if (const char* tv = std::getenv("ESCG_BLOCK_THREADS")) h->threads = std::atoi(tv) == 512 ? 512 : 1024;
             int kmax = escgd::kMaxBlockMcs;
             if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
             plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
             h->d_cur.alloc(n_replicas);
-            h->threads = 1024;
+            // persistent cooperative mode: every CTA co-resident, 16-aligned columns (TMA rows and
+            // vector stores) and a window that wraps at most once
+            // opt-in (ESCG_PERSISTENT=1): bit-identical results, one launch per run, but measured
+            // ~4% slower than one launch per chunk at L=3200 (grid.sync vs kernel boundary)
+            const bool env_off = !(std::getenv("ESCG_PERSISTENT") && std::string(std::getenv("ESCG_PERSISTENT")) == "1");
+            const bool geom_ok = h->L % 16 == 0 && h->bw_max % 16 == 0 &&
+                                 h->bh_max + 2 * escgd::margin_rows(h->kmcs) <= h->H &&
+                                 h->bw_max + 2 * escgd::margin_cols(h->kmcs) <= h->L;
+            if (!env_off && geom_ok) {
+                const int cap = escgd::block_persistent_capacity(h->arity, h->threads, h->smem, device);
+                h->persist = h->nby * h->nbx * n_replicas <= cap;
+            }
+            if (h->persist) h->d_acc3.alloc(static_cast<size_t>(3) * n_replicas * h->S1);
             h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
             h->d_ticket.alloc(n_replicas);
         }
@@ -754,6 +811,24 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
             launches = 1;
             timed_end(h, launches);
             for (auto& m : h->mcs) m += n_mcs;
+        } else if (h->persist) {
+            const escgd::RunArgs run = run_args(h, 0, 1, 0, 0, false);
+            CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t) * h->nrep, h->stream));
+            upload_mcs(h);
+            escgd::PersistArgs pa = persist_args(h, run);
+            pa.mcs0 = h->mcs[0];
+            pa.mcs_end = h->mcs[0] + n_mcs;
+            pa.record = 0;
+            timed_begin(h);
+            CK(escgd::launch_block_persistent(pa, h->nrep, h->threads, h->stream));
+            launches = 1;
+            timed_end(h, launches);
+            std::vector<int32_t> cur(h->nrep);
+            CK(cudaMemcpy(cur.data(), h->d_cur.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost));
+            for (int r = 0; r < h->nrep; ++r) {
+                h->mcs[r] += n_mcs;
+                h->cur[r] = cur[r];
+            }
         } else {
             const escgd::RunArgs run = run_args(h, 0, 1, 0, 0, false);
             CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t) * h->nrep, h->stream));
@@ -865,10 +940,11 @@ int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t*
     });
 }
 
-int escg_dev_block_mcs(escg_dev* h, int32_t* kmcs) {
+int escg_dev_block_mode(escg_dev* h, int32_t* kmcs, int32_t* persistent) {
     return guarded([&] {
-        if (!h || !kmcs) config_error("null argument");
-        *kmcs = h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1;
+        if (!h) config_error("null argument");
+        if (kmcs) *kmcs = h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1;
+        if (persistent) *persistent = (h->kernel == ESCG_KERNEL_BLOCK && h->persist) ? 1 : 0;
     });
 }
 

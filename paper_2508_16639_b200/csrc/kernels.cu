@@ -8,6 +8,7 @@
 //                 (overlapped tiling — counter-based draws make the redundant margin work
 //                 bit-identical across CTAs), and writes its block to the other buffer.
 //   init/count/replay/convert helpers.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -654,6 +655,134 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     DIAG_STAMP(9);
 }
 
+// Persistent variant: one cooperative launch runs every chunk of a run; a grid barrier replaces the
+// kernel boundary.  Records: CTAs add their block counts into acc3[r % 3]; after the barrier every
+// CTA reads the same totals and takes the same stop decision; CTA 0 writes the record and zeroes
+// acc3[(r + 2) % 3] (last read before the previous barrier, next written after the next one).
+template <int ARITY>
+__global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) uint8_t smem[];
+    const BlockArgs& a = pa.b;
+    const int r = blockIdx.z;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
+    const int kmax = pa.kmcs;
+    const int My = margin_rows(kmax), Mx = margin_cols(kmax);
+    const int ry0 = a.row_split[blockIdx.y], ry1 = a.row_split[blockIdx.y + 1];
+    const int rx0 = a.col_split[blockIdx.x], rx1 = a.col_split[blockIdx.x + 1];
+    const int bh = ry1 - ry0, bw = rx1 - rx0;
+    const size_t N = static_cast<size_t>(H) * L;
+    uint8_t* win = smem;
+    const int Whm = bh + 2 * My;
+    const int woff = (Whm * P + 15) & ~15;
+    uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
+    int2* tblp = reinterpret_cast<int2*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15));
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(tblp + 32);
+    uint8_t* sScratch = reinterpret_cast<uint8_t*>(sCnt + kMaxSpecies + 1);
+    __shared__ __align__(8) uint64_t sMbar;
+    const int nblk = gridDim.x * gridDim.y;  // CTAs per replica
+
+    const uint32_t s32 = seed32(a.seeds[r]);
+    for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+    build_offset_table<ARITY>(tblp, P);
+    for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
+    const uint32_t mbar = smem_addr(&sMbar);
+    if (tid == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint32_t win0 = smem_addr(win), tbl = smem_addr(tblp), sTa = smem_addr(sT);
+    const RunArgs& run = a.run;
+    const int64_t limit = pa.record ? run.mcs_limit : pa.mcs_end;
+    int64_t mcs = pa.mcs0;
+    int par = 0;       // buffer holding the lattice
+    int64_t rec = 0;   // record index
+    uint32_t tma_phase = 0;
+    bool running = true;
+
+    // record_and_check on the current lattice (block region in `src`, pitch `pitch`)
+    auto do_record = [&](const uint8_t* base, int pitch) {
+        for (int v = tid; v < S1; v += nt) sCnt[v] = 0;
+        __syncthreads();
+        block_count(base, bh, bw, pitch, S1, sCnt);
+        __syncthreads();
+        unsigned long long* acc = pa.acc3 + (static_cast<size_t>(rec % 3) * gridDim.z + r) * S1;
+        if (tid < S1 && sCnt[tid]) atomicAdd(&acc[tid], static_cast<unsigned long long>(sCnt[tid]));
+        grid.sync();
+        uint64_t c64[kMaxSpecies + 1];
+        int alive = 0;
+        for (int v = 0; v < S1; ++v) {
+            c64[v] = *reinterpret_cast<volatile unsigned long long*>(&acc[v]);
+            if (v >= 1 && c64[v] > 0) ++alive;
+        }
+        int st = kStatusRunning;
+        if ((run.stop_flags & kStopTracked) && run.tracked >= 1 && run.tracked < S1 && c64[run.tracked] == 0)
+            st = kStopped;
+        else if (mcs >= run.mcs_limit)
+            st = kCompleted;
+        else if ((run.stop_flags & kStopStasis) && alive <= 1)
+            st = kStasis;
+        if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+            record_decide(c64, S1, mcs, r, run);
+            if (run.cur) run.cur[r] = par;
+            unsigned long long* z = pa.acc3 + (static_cast<size_t>((rec + 2) % 3) * gridDim.z + r) * S1;
+            for (int v = 0; v < S1; ++v) z[v] = 0ull;
+        }
+        ++rec;
+        running = st == kStatusRunning;
+    };
+
+    if (pa.record) do_record(pa.buf[0] + r * N + static_cast<size_t>(ry0) * L + rx0, L);
+    int64_t next_rec = pa.record ? pa.mcs0 + run.interval : limit;
+    while (running && mcs < limit) {
+        const int64_t target = pa.record ? (next_rec < limit ? next_rec : limit) : limit;
+        const int chunk = static_cast<int>((target - mcs) < kmax ? (target - mcs) : kmax);
+        const int Myc = margin_rows(chunk), Mxc = margin_cols(chunk);
+        const int Wh = bh + 2 * Myc, Ww = bw + 2 * Mxc;
+        const int wy0 = ((ry0 - Myc) % H + H) % H;
+        const int wx0 = ((rx0 - Mxc) % L + L) % L;
+        const uint8_t* src = pa.buf[par] + r * N;
+        uint8_t* dst = pa.buf[1 - par] + r * N;
+        // generic-proxy writes of the previous chunk (other CTAs) → this CTA's async-proxy reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (tid == 0) mbar_expect_tx_arrive(mbar, static_cast<uint32_t>(Wh * Ww));
+        __syncthreads();
+        load_window_tma(win, src, H, L, P, Wh, Ww, wy0, wx0, mbar);
+        mbar_wait(mbar, tma_phase);
+        tma_phase ^= 1u;
+        __syncthreads();
+        BlockGeom g;
+        g.P = P;
+        g.H = H;
+        g.L = L;
+        g.nmcs = chunk;
+        g.mcs = mcs;
+        g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
+        if (a.narrow)
+            block_phases<ARITY, true>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+        else
+            block_phases<ARITY, false>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+        store_block<16>(dst, win, L, P, bh, bw, ry0, rx0, Myc, Mxc);
+        mcs += chunk;
+        par ^= 1;
+        if (pa.record && mcs == target) {
+            __threadfence();
+            do_record(win + Myc * P + Mxc, P);  // includes the grid barrier
+            next_rec = mcs + run.interval;
+        } else {
+            __threadfence();
+            grid.sync();
+        }
+    }
+    if (!pa.record && blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+        run.mcs[r] = mcs;
+        if (run.cur) run.cur[r] = par;
+    }
+}
+
 // ---------------------------------------------------------------------------------------------
 // Helpers
 // ---------------------------------------------------------------------------------------------
@@ -818,6 +947,29 @@ static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cud
     dim3 grid(static_cast<unsigned>(a.nbx), static_cast<unsigned>(a.nby), static_cast<unsigned>(nrep));
     k<<<grid, threads, a.smem_bytes, s>>>(a);
     return cudaGetLastError();
+}
+
+int block_persistent_capacity(int arity, int threads, int smem_bytes, int device) {
+    int per_sm = 0, sms = 0;
+    auto k4 = block_kernel_persistent<4>;
+    auto k8 = block_kernel_persistent<8>;
+    const void* f = arity == 8 ? reinterpret_cast<const void*>(k8) : reinterpret_cast<const void*>(k4);
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem_bytes) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int coop = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    return coop ? per_sm * sms : 0;
+}
+
+cudaError_t launch_block_persistent(const PersistArgs& a, int nrep, int threads, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>(a.b.nbx), static_cast<unsigned>(a.b.nby), static_cast<unsigned>(nrep));
+    void* args[] = {const_cast<PersistArgs*>(&a)};
+    const void* f = a.b.arity == 8 ? reinterpret_cast<const void*>(block_kernel_persistent<8>)
+                                   : reinterpret_cast<const void*>(block_kernel_persistent<4>);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, a.b.smem_bytes);
+    if (e != cudaSuccess) return e;
+    return cudaLaunchCooperativeKernel(f, grid, dim3(static_cast<unsigned>(threads)), args, a.b.smem_bytes, s);
 }
 
 cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {

@@ -74,6 +74,16 @@ struct BlockArgs {
     int smem_bytes;
 };
 
+// Persistent cooperative block kernel: the whole run/advance in one launch (all CTAs co-resident).
+struct PersistArgs {
+    BlockArgs b;              // geometry, rule, run bookkeeping, buffers (src = buffer 0 at start)
+    uint8_t* buf[2];
+    int64_t mcs0, mcs_end;    // advance: [mcs0, mcs_end); run: limit = b.run.mcs_limit
+    int record;               // 1: record/check loop at b.run.interval; 0: advance only
+    int kmcs;                 // MCS per chunk
+    unsigned long long* acc3; // [3][rep][S+1] record accumulators (zeroed by the host)
+};
+
 struct InitArgs {
     uint8_t* lat;
     const uint64_t* seeds;
@@ -98,6 +108,8 @@ cudaError_t launch_init(const InitArgs& a, cudaStream_t s);
 cudaError_t launch_count(const uint8_t* lat, int64_t n, int nrep, int S, unsigned long long* out, cudaStream_t s);
 cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s);
 cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t s);
+cudaError_t launch_block_persistent(const PersistArgs& a, int nrep, int threads, cudaStream_t s);
+int block_persistent_capacity(int arity, int threads, int smem_bytes, int device);
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
 cudaError_t launch_u8_to_i32(const uint8_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_i32_to_u8(const int32_t* src, uint8_t* dst, int64_t n, int S, int* bad, cudaStream_t s);

@@ -419,10 +419,10 @@ class DeviceEngine:
         vals = [C.c_int32(0) for _ in range(4)]
         check(lib().escg_dev_describe(self._h, *[C.byref(v) for v in vals]))
         kernel, ctas, threads, smem = (v.value for v in vals)
-        k = C.c_int32(0)
-        check(lib().escg_dev_block_mcs(self._h, C.byref(k)))
+        k, pers = C.c_int32(0), C.c_int32(0)
+        check(lib().escg_dev_block_mode(self._h, C.byref(k), C.byref(pers)))
         return dict(kernel={1: "tile", 2: "block"}[kernel], ctas=ctas, threads=threads, smem_bytes=smem,
-                    draw_format=self.draw_format(), kmcs=k.value)
+                    draw_format=self.draw_format(), kmcs=k.value, persistent=bool(pers.value))
 
 
 def thresholds(mobility: float, cells: int, model: DominanceModel):

@@ -263,3 +263,50 @@ def test_device_replica_runner_matches_single_engine(escg):
             eng.init_lattice()
             eng.run(30, interval=1, record_trace=False)
             assert eng.replica_result(0)[2].tolist() == counts and m == 30
+
+
+@pytest.mark.parametrize("LH,arity", [((320, 320), 4), ((256, 384), 8)])
+def test_persistent_block_kernel_matches_oracle_and_launch_path(escg, oracle, LH, arity, monkeypatch):
+    """Persistent cooperative mode (one launch per run, grid barrier between chunks) == oracle ==
+    one-launch-per-chunk mode, for advance and for run() with records."""
+    L, H = LH
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, H, 3, 3e-3, 0.1, arity, True, seed=321, mcs=11)
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ESCG_PERSISTENT", mode)
+        with escg.DeviceEngine(p, model, kernel="block") as eng:
+            d = eng.describe()
+            assert d["persistent"] == (mode == "1"), d
+            eng.init_lattice()
+            init = eng.get_lattice()
+            eng.advance(5)
+            a5 = eng.get_lattice()
+            st = eng.run(11, interval=3)
+            steps, counts = eng.read_trace()
+            outs[mode] = (a5, eng.get_lattice(), steps.tolist(), counts.tolist(), int(st[0]), eng.mcs(),
+                          eng.draw_format() == "narrow")
+    assert all((np.array_equal(x, y) if isinstance(x, np.ndarray) else x == y)
+               for x, y in zip(outs["1"][:6], outs["0"][:6]))
+    a5, fin, steps, counts, st, m, narrow = outs["1"]
+    assert steps == [5, 8, 11] and st == int(escg.RunStatus.Completed) and m == 11
+    want5 = oracle.crs_run(init, L, H, model.matrix(), 3e-3, 321, 0, 5, arity=arity, narrow=narrow)
+    assert np.array_equal(a5, want5)
+    want11 = oracle.crs_run(want5, L, H, model.matrix(), 3e-3, 321, 5, 6, arity=arity, narrow=narrow)
+    assert np.array_equal(fin, want11)
+    assert counts[-1] == oracle.densities(want11, 3).tolist()
+
+
+def test_persistent_tracked_stop(escg, monkeypatch):
+    """Early stop inside a persistent run: ablated RPSLS until Paper dies; same MCS/lattice as the
+    per-launch path."""
+    res = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ESCG_PERSISTENT", mode)
+        p = params(escg, 256, 256, 5, 3e-4, 0.0, 4, True, seed=9, mcs=3000)
+        with escg.DeviceEngine(p, escg.make_rpsls_ablated(), kernel="block") as eng:
+            eng.init_lattice()
+            st = eng.run(3000, interval=1, tracked=4)
+            res[mode] = (int(st[0]), eng.mcs(), eng.get_lattice(), eng.read_trace()[1][-1].tolist())
+    assert res["1"][0] == res["0"][0] and res["1"][1] == res["0"][1]
+    assert np.array_equal(res["1"][2], res["0"][2]) and res["1"][3] == res["0"][3]
