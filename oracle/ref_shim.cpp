@@ -240,3 +240,42 @@ EXPORT double ref_ks_two_sample_pvalue(const double* a, std::int64_t na, const d
 EXPORT double ref_chi_square_uniform_pvalue(const std::uint64_t* bins, std::int64_t n) {
     return escg::chi_square_uniform_pvalue(std::vector<std::uint64_t>(bins, bins + n));
 }
+
+// persistence.cpp:57-62 format_double (std::to_chars shortest round-trip), for the CSV formats.
+#include "escg/persistence.hpp"
+EXPORT int ref_format_double(double v, char* buf, int cap) {
+    const std::string s = escg::format_double(v);
+    if (static_cast<int>(s.size()) + 1 > cap) return -1;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
+}
+
+// experiments.cpp:242-285 CSV writers on caller data (format pins for the device harness).
+#include "escg/experiments.hpp"
+EXPORT int ref_write_extinction_csv(const std::int64_t* times, const int* censored, int n, const char* path) {
+    try {
+        escg::ExtinctionStats st;
+        for (int i = 0; i < n; ++i) {
+            st.times.push_back(times[i]);
+            st.censored.push_back(censored[i] != 0);
+        }
+        escg::write_extinction_csv(st, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+EXPORT int ref_write_coexistence_csv(int trials, int coexisting, double probability, double mobility, int length,
+                                     std::int64_t mcs, const char* path) {
+    try {
+        escg::CoexistenceResult r;
+        r.trials = trials;
+        r.coexisting = coexisting;
+        r.probability = probability;
+        escg::write_coexistence_csv(r, mobility, length, mcs, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
