@@ -154,6 +154,16 @@ ESCG_API int escg_dev_draw_format(escg_dev* h, int32_t* narrow);
  * executes as one persistent cooperative launch (1) or one launch per chunk (0). */
 ESCG_API int escg_dev_block_mode(escg_dev* h, int32_t* kmcs, int32_t* persistent);
 
+/* Row-band sharding of one lattice.  Band `band` of `n_bands` (rows split at
+ * multiples of 4) with halo = 12*kmcs rows on each side; draws use global coordinates, so a band
+ * group reproduces the single-lattice run bit-for-bit.  set/get/counts address the band rows. */
+ESCG_API int escg_dev_create_band(const escg_params* p, const double* dominance, int32_t species, int32_t kind,
+                                  int32_t device, int32_t n_bands, int32_t band, int32_t kmcs, escg_dev** out);
+ESCG_API int escg_dev_band_info(escg_dev* h, int32_t* band_start, int32_t* band_rows, int32_t* halo, int32_t* kmcs);
+/* Advance a whole band group (bands[g] = band g; any mix of devices) by n_mcs: per chunk, halo
+ * exchange by peer copies between ring neighbours, then the block kernel on every band. */
+ESCG_API int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs);
+
 /* One-call mirror of escg::simulate(params, model, mode, …) (engine.cpp:194-240) for a single
  * lattice: initialise on device (or resume from resume_cells at resume_mcs), run to completion
  * under `mode`'s record cadence with the device stop predicates, return the final int32 lattice,

@@ -1,0 +1,106 @@
+"""Row-band sharding of one lattice over several GPUs.
+
+Band g owns rows [start_g, start_g + rows_g) (multiples of 4) of the global lattice and keeps
+12*kmcs halo rows on each side.  Every chunk of kmcs MCS each band pulls its halos from its ring
+neighbours (peer copies over NVLink when the bands sit on different GPUs) and runs the block kernel
+on its rows.  The draws are a function of the global (seed, MCS, phase, tile), so the banded run is
+bit-identical to the single-lattice run for any number of bands (tests/test_gpu_parity.py).
+
+`BandGroup` drives all bands from one process (one GPU or several with peer access).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import numpy as np
+
+from ._lib import check, lib
+from .engine import DominanceModel, SimParams
+from .errors import ConfigError
+
+
+def band_rows(height: int, n_bands: int):
+    """Row split of the band engines (engine.cpp create_impl): [(start, rows)] at multiples of 4."""
+    u = height // 4
+    return [(u * g // n_bands * 4, (u * (g + 1) // n_bands - u * g // n_bands) * 4) for g in range(n_bands)]
+
+
+class BandGroup:
+    def __init__(self, params: SimParams, model: DominanceModel, n_bands: int, devices: Optional[Sequence[int]] = None,
+                 kmcs: int = 2):
+        if params.seed is None:
+            raise ConfigError("a band group needs an explicit seed (every band must share it)")
+        self.params, self.model, self.n = params, model, int(n_bands)
+        devices = list(devices) if devices is not None else [0] * self.n
+        if len(devices) != self.n:
+            raise ConfigError("one device per band")
+        self._h = []
+        try:
+            for g in range(self.n):
+                h = C.c_void_p()
+                check(lib().escg_dev_create_band(C.byref(params.to_c()), np.ascontiguousarray(model.entries, np.float64),
+                                                 int(model.size), int(model.kind), int(devices[g]), self.n, g,
+                                                 int(kmcs), C.byref(h)))
+                self._h.append(h)
+        except Exception:
+            self.close()
+            raise
+        self.info = [self._band_info(h) for h in self._h]
+
+    @staticmethod
+    def _band_info(h):
+        v = [C.c_int32(0) for _ in range(4)]
+        check(lib().escg_dev_band_info(h, *[C.byref(x) for x in v]))
+        return dict(start=v[0].value, rows=v[1].value, halo=v[2].value, kmcs=v[3].value)
+
+    def close(self):
+        for h in self._h:
+            if h:
+                lib().escg_dev_destroy(h)
+        self._h = []
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def init_lattice(self):
+        for h in self._h:
+            check(lib().escg_dev_init_lattice(h))
+
+    def set_lattice(self, cells, mcs: int = 0):
+        cells = np.ascontiguousarray(np.asarray(cells).ravel(), np.int32)
+        L = self.params.length
+        for h, inf in zip(self._h, self.info):
+            part = np.ascontiguousarray(cells[inf["start"] * L:(inf["start"] + inf["rows"]) * L])
+            check(lib().escg_dev_set_lattice(h, 0, part, int(mcs)))
+
+    def get_lattice(self) -> np.ndarray:
+        L = self.params.length
+        out = np.zeros(self.params.cells(), np.int32)
+        for h, inf in zip(self._h, self.info):
+            part = np.zeros(inf["rows"] * L, np.int32)
+            m = C.c_int64(0)
+            check(lib().escg_dev_get_lattice(h, 0, part.ctypes.data_as(C.c_void_p), C.byref(m)))
+            out[inf["start"] * L:(inf["start"] + inf["rows"]) * L] = part
+        return out
+
+    def counts(self) -> np.ndarray:
+        tot = np.zeros(self.model.size + 1, np.uint64)
+        for h in self._h:
+            c = np.zeros(self.model.size + 1, np.uint64)
+            check(lib().escg_dev_counts(h, 0, c))
+            tot += c
+        return tot
+
+    def advance(self, n_mcs: int):
+        arr = (C.c_void_p * self.n)(*[h.value for h in self._h])
+        check(lib().escg_group_advance(arr, self.n, int(n_mcs)))

@@ -186,6 +186,11 @@ struct escg_dev {
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
     int bh_max = 0, bw_max = 0;
+    // row-band engines (one band of a lattice sharded by rows): the local buffer holds
+    // halo + band_rows + halo rows; local row r is global row (row0 + r) mod Hg
+    int Hg = 0, row0 = 0, wrap_rows = 1;
+    int nbands = 1, band = 0, band_start = 0, band_rows = 0, halo = 0;
+    int rows_begin = 0, rows_count = 0;  // rows of the local buffer the engine owns (blocks, I/O)
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_poll = nullptr;
     int32_t* h_status = nullptr;  // pinned, status polling of the block path
@@ -241,7 +246,7 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     sms *= cta_per_sm;
     smem_cap = std::min(smem_cap, (228 * 1024) / cta_per_sm - 1024);
     const int cu = (h->L % 16 == 0) ? 16 : ((h->L % 8 == 0) ? 8 : 4);
-    const int uy = h->H / 4, ux = h->L / cu;
+    const int uy = h->rows_count / 4, ux = h->L / cu;
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
     const double kOverheadCells = 40000.0;  // launch + window load/store, measured on B200
@@ -267,7 +272,7 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     h->nbx = bnbx;
     h->kmcs = bk;
     std::vector<int> rows(bnby + 1), cols(bnbx + 1);
-    for (int i = 0; i <= bnby; ++i) rows[i] = static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
+    for (int i = 0; i <= bnby; ++i) rows[i] = h->rows_begin + static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
     for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(ux) * i / bnbx) * cu;
     int bh = 0, bw = 0;
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
@@ -322,6 +327,10 @@ uint8_t* replica_lat(escg_dev* h, int r) {
     return h->lat[h->kernel == ESCG_KERNEL_BLOCK ? h->cur[r] : 0].p + static_cast<size_t>(r) * h->N;
 }
 
+// The rows an engine owns (whole lattice, or the band of a band engine): I/O and counts use these.
+uint8_t* owned_lat(escg_dev* h, int r) { return replica_lat(h, r) + static_cast<size_t>(h->rows_begin) * h->L; }
+int64_t owned_cells(escg_dev* h) { return static_cast<int64_t>(h->rows_count) * h->L; }
+
 void check_replica(escg_dev* h, int r) {
     if (r < 0 || r >= h->nrep) config_error("replica index out of range");
 }
@@ -350,6 +359,9 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.P = h->P;
     a.arity = h->arity;
     a.narrow = h->narrow;
+    a.Hg = h->Hg;
+    a.row0 = h->row0;
+    a.wrap_rows = h->wrap_rows;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -388,6 +400,9 @@ escgd::PersistArgs persist_args(escg_dev* h, const escgd::RunArgs& run) {
     a.P = h->P;
     a.arity = h->arity;
     a.narrow = h->narrow;
+    a.Hg = h->Hg;
+    a.row0 = h->row0;
+    a.wrap_rows = h->wrap_rows;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -471,6 +486,9 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.P = h->P;
         a.arity = h->arity;
         a.narrow = h->narrow;
+        a.Hg = h->Hg;
+        a.row0 = h->row0;
+        a.wrap_rows = h->wrap_rows;
         a.nby = h->nby;
         a.nbx = h->nbx;
         a.row_split = h->d_rows.p;
@@ -585,9 +603,43 @@ int64_t escg_align_num_randoms(int64_t requested, int64_t cells) {
     return rc == ESCG_OK ? out : -1;
 }
 
+}  // extern "C"
+
+namespace {
+struct BandSpec {
+    int nbands = 1, band = 0, kmcs = 2;
+};
+
+void create_impl(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t device,
+                 int32_t n_replicas, const uint64_t* replica_seeds, int32_t kernel, escg_dev** out,
+                 const BandSpec* bs);
+}  // namespace
+
+extern "C" {
+
 int escg_dev_create(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t device,
                     int32_t n_replicas, const uint64_t* replica_seeds, int32_t kernel, escg_dev** out) {
+    return guarded([&] { create_impl(p, dominance, species, kind, device, n_replicas, replica_seeds, kernel, out, nullptr); });
+}
+
+int escg_dev_create_band(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t device,
+                         int32_t n_bands, int32_t band, int32_t kmcs, escg_dev** out) {
     return guarded([&] {
+        BandSpec bs;
+        bs.nbands = n_bands;
+        bs.band = band;
+        bs.kmcs = kmcs > 0 ? kmcs : 2;
+        create_impl(p, dominance, species, kind, device, 1, nullptr, ESCG_KERNEL_BLOCK, out, &bs);
+    });
+}
+
+}  // extern "C"
+
+namespace {
+void create_impl(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t device,
+                 int32_t n_replicas, const uint64_t* replica_seeds, int32_t kernel, escg_dev** out,
+                 const BandSpec* bs) {
+    {
         if (!p || !out) config_error("null argument");
         *out = nullptr;
         validate_params(*p);
@@ -622,6 +674,33 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
         h->x_empty = empty_threshold(p->empty_prob);
         h->mcs.assign(n_replicas, 0);
         h->cur.assign(n_replicas, 0);
+        h->Hg = h->H;
+        h->rows_begin = 0;
+        h->rows_count = h->H;
+        if (bs) {
+            // band `band` of `nbands` row bands (multiples of 4 rows) plus halo rows on both sides
+            if (bs->nbands < 2) config_error("a band engine needs at least 2 bands");
+            if (bs->band < 0 || bs->band >= bs->nbands) config_error("band index out of range");
+            if (bs->kmcs < 1 || bs->kmcs > escgd::kMaxBlockMcs) config_error("band chunk (kmcs) must be in [1, 4]");
+            if (!(h->flux && h->H % 4 == 0 && h->L % 4 == 0)) config_error("band sharding needs a periodic lattice with L, H divisible by 4");
+            if (n_replicas != 1) config_error("band engines hold one lattice");
+            const int u = h->H / 4;
+            h->nbands = bs->nbands;
+            h->band = bs->band;
+            h->band_start = static_cast<int>(static_cast<int64_t>(u) * bs->band / bs->nbands) * 4;
+            h->band_rows = static_cast<int>(static_cast<int64_t>(u) * (bs->band + 1) / bs->nbands) * 4 - h->band_start;
+            h->halo = escgd::margin_rows(bs->kmcs);
+            if (h->band_rows < h->halo)
+                config_error("band too thin for the halo (" + std::to_string(h->band_rows) + " rows < " +
+                             std::to_string(h->halo) + "): use fewer bands or a smaller chunk");
+            h->H = h->band_rows + 2 * h->halo;
+            h->N = static_cast<int64_t>(h->H) * h->L;
+            h->row0 = ((h->band_start - h->halo) % h->Hg + h->Hg) % h->Hg;
+            h->wrap_rows = 0;
+            h->rows_begin = h->halo;
+            h->rows_count = h->band_rows;
+            h->kmcs = bs->kmcs;
+        }
 
         cudaDeviceProp prop{};
         CK(cudaGetDeviceProperties(&prop, device));
@@ -667,6 +746,7 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
             if (const char* tv = std::getenv("ESCG_BLOCK_THREADS")) h->threads = std::atoi(tv) == 512 ? 512 : 1024;
             int kmax = escgd::kMaxBlockMcs;
             if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
+            if (bs) kmax = bs->kmcs;  // chunks may not outgrow the band's halo
             plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
             h->d_cur.alloc(n_replicas);
             // persistent cooperative mode: every CTA co-resident, 16-aligned columns (TMA rows and
@@ -677,7 +757,7 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
             const bool geom_ok = h->L % 16 == 0 && h->bw_max % 16 == 0 &&
                                  h->bh_max + 2 * escgd::margin_rows(h->kmcs) <= h->H &&
                                  h->bw_max + 2 * escgd::margin_cols(h->kmcs) <= h->L;
-            if (!env_off && geom_ok) {
+            if (!env_off && geom_ok && h->wrap_rows) {
                 const int cap = escgd::block_persistent_capacity(h->arity, h->threads, h->smem, device);
                 h->persist = h->nby * h->nbx * n_replicas <= cap;
             }
@@ -699,8 +779,11 @@ int escg_dev_create(const escg_params* p, const double* dominance, int32_t speci
         CK(cudaMemset(h->d_nrec.p, 0, sizeof(int64_t) * n_replicas));
         CK(cudaMemset(h->d_last.p, 0, sizeof(uint64_t) * h->S1 * n_replicas));
         *out = h.release();
-    });
+    }
 }
+}  // namespace
+
+extern "C" {
 
 int escg_dev_destroy(escg_dev* h) {
     return guarded([&] {
@@ -718,6 +801,9 @@ int escg_dev_init_lattice(escg_dev* h) {
         a.lat = h->lat[0].p;
         a.seeds = h->d_seeds.p;
         a.n = h->N;
+        a.L = h->L;
+        a.Hg = h->Hg;
+        a.row0 = h->row0;
         a.nrep = h->nrep;
         a.S = h->S;
         a.x_empty = h->x_empty;
@@ -735,10 +821,11 @@ int escg_dev_set_lattice(escg_dev* h, int32_t replica, const int32_t* cells, int
         check_replica(h, replica);
         if (mcs < 0) config_error("mcs must be non-negative");
         CK(cudaSetDevice(h->device));
-        if (h->d_i32.n < static_cast<size_t>(h->N)) h->d_i32.alloc(h->N);
-        CK(cudaMemcpyAsync(h->d_i32.p, cells, sizeof(int32_t) * h->N, cudaMemcpyHostToDevice, h->stream));
+        const int64_t n = owned_cells(h);
+        if (h->d_i32.n < static_cast<size_t>(n)) h->d_i32.alloc(n);
+        CK(cudaMemcpyAsync(h->d_i32.p, cells, sizeof(int32_t) * n, cudaMemcpyHostToDevice, h->stream));
         CK(cudaMemsetAsync(h->d_bad.p, 0, sizeof(int), h->stream));
-        CK(escgd::launch_i32_to_u8(h->d_i32.p, replica_lat(h, replica), h->N, h->S, h->d_bad.p, h->stream));
+        CK(escgd::launch_i32_to_u8(h->d_i32.p, owned_lat(h, replica), n, h->S, h->d_bad.p, h->stream));
         int bad = 0;
         CK(cudaMemcpyAsync(&bad, h->d_bad.p, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
@@ -753,9 +840,10 @@ int escg_dev_get_lattice(escg_dev* h, int32_t replica, int32_t* out, int64_t* mc
         check_replica(h, replica);
         CK(cudaSetDevice(h->device));
         if (out) {
-            if (h->d_i32.n < static_cast<size_t>(h->N)) h->d_i32.alloc(h->N);
-            CK(escgd::launch_u8_to_i32(replica_lat(h, replica), h->d_i32.p, h->N, h->stream));
-            CK(cudaMemcpyAsync(out, h->d_i32.p, sizeof(int32_t) * h->N, cudaMemcpyDeviceToHost, h->stream));
+            const int64_t n = owned_cells(h);
+            if (h->d_i32.n < static_cast<size_t>(n)) h->d_i32.alloc(n);
+            CK(escgd::launch_u8_to_i32(owned_lat(h, replica), h->d_i32.p, n, h->stream));
+            CK(cudaMemcpyAsync(out, h->d_i32.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, h->stream));
             CK(cudaStreamSynchronize(h->stream));
         }
         if (mcs_out) *mcs_out = h->mcs[replica];
@@ -769,7 +857,7 @@ int escg_dev_counts(escg_dev* h, int32_t replica, uint64_t* out) {
         CK(cudaSetDevice(h->device));
         DevBuf<unsigned long long> tmp;
         tmp.alloc(h->S1);
-        CK(escgd::launch_count(replica_lat(h, replica), h->N, 1, h->S, tmp.p, h->stream));
+        CK(escgd::launch_count(owned_lat(h, replica), owned_cells(h), 1, h->S, tmp.p, h->stream));
         CK(cudaMemcpyAsync(out, tmp.p, sizeof(uint64_t) * h->S1, cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
     });
@@ -778,6 +866,7 @@ int escg_dev_counts(escg_dev* h, int32_t replica, uint64_t* out) {
 int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
     return guarded([&] {
         if (!h) config_error("null handle");
+        if (h->nbands > 1) config_error("band engines advance through escg_group_advance");
         if (n_mcs < 0) config_error("mcs count must be non-negative");
         CK(cudaSetDevice(h->device));
         normalize_buffers(h);
@@ -850,6 +939,7 @@ int escg_dev_run(escg_dev* h, int64_t mcs_limit, int64_t interval, uint32_t stop
                  int32_t record_trace, int32_t* status_out) {
     return guarded([&] {
         if (!h) config_error("null handle");
+        if (h->nbands > 1) config_error("band engines advance through escg_group_advance");
         CK(cudaSetDevice(h->device));
         const std::vector<int64_t> start(h->mcs);
         run_impl(h, mcs_limit, interval, stop_flags, tracked_species, record_trace != 0, status_out);
@@ -945,6 +1035,131 @@ int escg_dev_block_mode(escg_dev* h, int32_t* kmcs, int32_t* persistent) {
         if (!h) config_error("null argument");
         if (kmcs) *kmcs = h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1;
         if (persistent) *persistent = (h->kernel == ESCG_KERNEL_BLOCK && h->persist) ? 1 : 0;
+    });
+}
+
+int escg_dev_band_info(escg_dev* h, int32_t* band_start, int32_t* band_rows, int32_t* halo, int32_t* kmcs) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (band_start) *band_start = h->nbands > 1 ? h->band_start : 0;
+        if (band_rows) *band_rows = h->nbands > 1 ? h->band_rows : h->H;
+        if (halo) *halo = h->nbands > 1 ? h->halo : 0;
+        if (kmcs) *kmcs = h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1;
+    });
+}
+
+// One group of band engines (one band each, any devices): chunks of k MCS; before each chunk every
+// band pulls its halo rows from its two ring neighbours' current buffers (cudaMemcpyPeerAsync), then
+// runs the block kernel on its band.  Streams are ordered with events, so bands on different GPUs
+// overlap; on one GPU the group is the bit-exact single-process reference of the sharded run.
+int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
+    return guarded([&] {
+        if (!bands || n < 2) config_error("a band group needs at least 2 bands");
+        if (n_mcs < 0) config_error("mcs count must be non-negative");
+        for (int g = 0; g < n; ++g) {
+            escg_dev* h = bands[g];
+            if (!h || h->nbands != n || h->band != g) config_error("group must list bands 0..n-1 of one lattice");
+            if (h->mcs[0] != bands[0]->mcs[0] || h->cur[0] != bands[0]->cur[0] || h->kmcs != bands[0]->kmcs)
+                config_error("bands are out of step");
+        }
+        // peer access between ring neighbours on different GPUs (NVLink P2P copies)
+        for (int g = 0; g < n; ++g) {
+            for (int nb : {(g + n - 1) % n, (g + 1) % n}) {
+                const int d0 = bands[g]->device, d1 = bands[nb]->device;
+                int can = 0;
+                if (d0 != d1 && cudaDeviceCanAccessPeer(&can, d0, d1) == cudaSuccess && can) {
+                    CK(cudaSetDevice(d0));
+                    const cudaError_t pe = cudaDeviceEnablePeerAccess(d1, 0);
+                    if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CK(pe);
+                    cudaGetLastError();  // clear "already enabled"
+                }
+            }
+        }
+        std::vector<cudaEvent_t> ev_k(n), ev_x(n);
+        for (int g = 0; g < n; ++g) {
+            CK(cudaSetDevice(bands[g]->device));
+            CK(cudaEventCreateWithFlags(&ev_k[g], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ev_x[g], cudaEventDisableTiming));
+            CK(cudaEventRecord(ev_k[g], bands[g]->stream));
+        }
+        const int64_t t0 = bands[0]->mcs[0];
+        int64_t launch_no = 0;
+        int par = bands[0]->cur[0];
+        const int k = bands[0]->kmcs;
+        for (int64_t done = 0; done < n_mcs;) {
+            const int chunk = static_cast<int>(std::min<int64_t>(k, n_mcs - done));
+            // halo exchange into buffer `par` (reads the neighbours' band rows of buffer `par`)
+            for (int g = 0; g < n; ++g) {
+                escg_dev* h = bands[g];
+                escg_dev* up = bands[(g + n - 1) % n];
+                escg_dev* dn = bands[(g + 1) % n];
+                CK(cudaSetDevice(h->device));
+                CK(cudaStreamWaitEvent(h->stream, ev_k[(g + n - 1) % n], 0));
+                CK(cudaStreamWaitEvent(h->stream, ev_k[(g + 1) % n], 0));
+                const size_t rowb = static_cast<size_t>(h->L);
+                const size_t hb = static_cast<size_t>(h->halo) * rowb;
+                uint8_t* mine = h->lat[par].p;
+                // top halo ← the last `halo` rows of the band above; bottom halo ← the first rows below
+                CK(cudaMemcpyPeerAsync(mine, h->device,
+                                       up->lat[par].p + static_cast<size_t>(up->halo + up->band_rows - h->halo) * rowb,
+                                       up->device, hb, h->stream));
+                CK(cudaMemcpyPeerAsync(mine + static_cast<size_t>(h->halo + h->band_rows) * rowb, h->device,
+                                       dn->lat[par].p + static_cast<size_t>(dn->halo) * rowb, dn->device, hb,
+                                       h->stream));
+                CK(cudaEventRecord(ev_x[g], h->stream));
+            }
+            // chunk: src = buffer par, dst = 1 - par.  A band's kernel overwrites buffer 1-par, which
+            // its neighbours read during the previous exchange: wait for their exchange events.
+            for (int g = 0; g < n; ++g) {
+                escg_dev* h = bands[g];
+                CK(cudaSetDevice(h->device));
+                CK(cudaStreamWaitEvent(h->stream, ev_x[(g + n - 1) % n], 0));
+                CK(cudaStreamWaitEvent(h->stream, ev_x[(g + 1) % n], 0));
+                const escgd::RunArgs run = run_args(h, 0, 1, 0, 0, false);
+                escgd::BlockArgs a{};
+                a.seeds = h->d_seeds.p;
+                a.rule = rule_args(h);
+                a.run = run;
+                a.H = h->H;
+                a.L = h->L;
+                a.S = h->S;
+                a.P = h->P;
+                a.arity = h->arity;
+                a.narrow = h->narrow;
+                a.Hg = h->Hg;
+                a.row0 = h->row0;
+                a.wrap_rows = h->wrap_rows;
+                a.nby = h->nby;
+                a.nbx = h->nbx;
+                a.row_split = h->d_rows.p;
+                a.col_split = h->d_cols.p;
+                a.acc = h->d_acc.p;
+                a.ticket = h->d_ticket.p;
+                a.smem_bytes = h->smem;
+                a.step = 1;
+                a.count = 0;
+                a.src = h->lat[par].p;
+                a.dst = h->lat[1 - par].p;
+                a.dst_index = 1 - par;
+                a.mcs = t0 + done;
+                a.nmcs = chunk;
+                CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
+                CK(escgd::launch_block(a, 1, h->threads, h->stream));
+                CK(cudaEventRecord(ev_k[g], h->stream));
+            }
+            par ^= 1;
+            done += chunk;
+            ++launch_no;
+        }
+        for (int g = 0; g < n; ++g) {
+            CK(cudaSetDevice(bands[g]->device));
+            CK(cudaStreamSynchronize(bands[g]->stream));
+            CK(cudaEventDestroy(ev_k[g]));
+            CK(cudaEventDestroy(ev_x[g]));
+            bands[g]->mcs[0] += n_mcs;
+            bands[g]->cur[0] = par;
+            bands[g]->last_launches = launch_no;
+        }
     });
 }
 

@@ -345,6 +345,7 @@ __device__ __forceinline__ int wrap_down(int v, int n, bool big) {
 // memory).
 struct BlockGeom {
     int P, H, L, nmcs;
+    int Hg, row0;      // global rows / global row of local row 0 (draws use global tile ids)
     int64_t mcs;
     uint32_t scratch;  // smem address of a dummy 4-row box (edge items with one invalid tile)
 };
@@ -353,10 +354,11 @@ template <int ARITY, bool NARROW>
 __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs rule, uint32_t win0, uint32_t tbl,
                                              uint32_t sT, int S1, int Wh, int Ww, int wy0, int wx0, uint32_t s32) {
     const int tid = threadIdx.x, nt = blockDim.x, P = g.P;
-    const int Ty = g.H >> 1, Tx = g.L >> 1, TQ = g.L >> 3;
-    const int jb = wy0 >> 1, ib = wx0 >> 1;  // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
+    const int Ty = g.Hg >> 1, Tx = g.L >> 1, TQ = g.L >> 3;
+    // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
+    const int jb = ((g.row0 + wy0) % g.Hg) >> 1, ib = wx0 >> 1;
     const int ex = margin_cols(g.nmcs) - margin_rows(g.nmcs);  // extra loaded columns
-    const bool big = Wh > g.H || Ww > g.L;  // window wraps more than once: use a true modulo
+    const bool big = Wh > g.Hg || Ww > g.L;  // window wraps more than once: use a true modulo
 #pragma unroll 1
     for (int t = 0; t < g.nmcs; ++t) {
         const uint64_t mcs = static_cast<uint64_t>(g.mcs + t);
@@ -569,7 +571,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
 
     if (a.step) {
         const uint32_t s32 = seed32(a.seeds[r]);
-        const int wy0 = ((ry0 - My) % H + H) % H;
+        const int wy0 = a.wrap_rows ? ((ry0 - My) % H + H) % H : ry0 - My;  // bands: halo rows, no wrap
         const int wx0 = ((rx0 - Mx) % L + L) % L;
         const uint32_t mbar = smem_addr(&sMbar);
 #ifndef ESCG_DIAG_NO_LOAD
@@ -602,6 +604,8 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         g.P = P;
         g.H = H;
         g.L = L;
+        g.Hg = a.Hg;
+        g.row0 = a.row0;
         g.nmcs = a.nmcs;
         g.mcs = a.mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
@@ -758,6 +762,8 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
         g.P = P;
         g.H = H;
         g.L = L;
+        g.Hg = a.Hg;
+        g.row0 = a.row0;
         g.nmcs = chunk;
         g.mcs = mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
@@ -797,12 +803,15 @@ __global__ void init_kernel(InitArgs a) {
         const int r = static_cast<int>(t / pairs);
         const int64_t pi = t - static_cast<int64_t>(r) * pairs;
         uint8_t* lat = a.lat + static_cast<size_t>(r) * a.n;
-        const uint4 w = philox(static_cast<uint32_t>(pi), 0u, ctr2(0, kDomInit, 0u, 0u), seed32(a.seeds[r]));
         const uint32_t S = static_cast<uint32_t>(a.S);
         for (int h = 0; h < 2; ++h) {
             const int64_t i = 2 * pi + h;
             if (i >= a.n) break;
-            const uint32_t we = h ? w.z : w.x, ws = h ? w.w : w.y;
+            // global cell index of local cell i (band engines start at global row row0)
+            const int64_t lr = i / a.L, col = i - lr * a.L;
+            const int64_t gi = ((a.row0 + lr) % a.Hg) * a.L + col;
+            const uint4 w = philox(static_cast<uint32_t>(gi >> 1), 0u, ctr2(0, kDomInit, 0u, 0u), seed32(a.seeds[r]));
+            const uint32_t we = (gi & 1) ? w.z : w.x, ws = (gi & 1) ? w.w : w.y;
             uint8_t v = 0;
             if (!a.all_empty && we >= a.x_empty) v = static_cast<uint8_t>(ws % S + 1u);
             lat[i] = v;

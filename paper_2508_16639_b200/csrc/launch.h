@@ -58,9 +58,12 @@ struct BlockArgs {
     const uint64_t* seeds;
     RuleArgs rule;
     RunArgs run;
-    int H, L, S, P;      // P = window pitch
+    int H, L, S, P;      // P = window pitch; H = rows of the local buffer
     int arity;
     int narrow;
+    int Hg;              // rows of the global lattice (tile ids / draws are global)
+    int row0;            // global row of local row 0 (band engines: band start - halo, mod Hg)
+    int wrap_rows;       // 1: the local buffer is the whole periodic lattice; 0: band with halo rows
     int nby, nbx;
     const int* row_split;  // nby+1 row boundaries (multiples of 4)
     const int* col_split;  // nbx+1
@@ -87,7 +90,10 @@ struct PersistArgs {
 struct InitArgs {
     uint8_t* lat;
     const uint64_t* seeds;
-    int64_t n;          // cells per replica
+    int64_t n;          // cells per replica (local buffer)
+    int L;              // row length
+    int Hg;             // global rows; local row r is global row (row0 + r) mod Hg
+    int row0;
     int nrep;
     int S;
     uint32_t x_empty;   // cell empty iff first word < x_empty (empty_prob test, lattice.hpp:59)

@@ -310,3 +310,47 @@ def test_persistent_tracked_stop(escg, monkeypatch):
             res[mode] = (int(st[0]), eng.mcs(), eng.get_lattice(), eng.read_trace()[1][-1].tolist())
     assert res["1"][0] == res["0"][0] and res["1"][1] == res["0"][1]
     assert np.array_equal(res["1"][2], res["0"][2]) and res["1"][3] == res["0"][3]
+
+
+@pytest.mark.parametrize("n_bands,kmcs,LH", [(2, 1, (96, 128)), (3, 2, (160, 160)), (4, 1, (200, 208)), (2, 2, (320, 192))])
+def test_band_group_equals_single_lattice(escg, oracle, n_bands, kmcs, LH):
+    """Row-band sharding (virtual bands on one GPU): bit-identical to the single-lattice engine and
+    to the oracle schedule — halos, global tile ids and init offsets are exact."""
+    from paper_2508_16639_b200.bands import BandGroup
+
+    L, H = LH
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, H, 3, 1e-2, 0.1, 4, True, seed=555)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(7)
+        single = eng.get_lattice()
+        narrow = eng.draw_format() == "narrow"
+    with BandGroup(p, model, n_bands, kmcs=kmcs) as grp:
+        grp.init_lattice()
+        assert np.array_equal(grp.get_lattice(), init)
+        grp.advance(3)
+        grp.advance(4)
+        banded = grp.get_lattice()
+        assert np.array_equal(grp.counts(), np.bincount(banded, minlength=4).astype(np.uint64))
+    assert np.array_equal(banded, single)
+    assert np.array_equal(single, oracle.crs_run(init, L, H, model.matrix(), 1e-2, 555, 0, 7, narrow=narrow))
+
+
+def test_band_group_resume_from_host_lattice(escg):
+    from paper_2508_16639_b200.bands import BandGroup
+
+    L, H = 128, 128
+    model = escg.make_rpsls()
+    p = params(escg, L, H, 5, 3e-3, 0.0, 8, True, seed=77)
+    rng = np.random.default_rng(1)
+    start = rng.integers(0, 6, L * H).astype(np.int32)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        eng.set_lattice(start, mcs=40)
+        eng.advance(6)
+        single = eng.get_lattice()
+    with BandGroup(p, model, 3, kmcs=2) as grp:
+        grp.set_lattice(start, mcs=40)
+        grp.advance(6)
+        assert np.array_equal(grp.get_lattice(), single)
