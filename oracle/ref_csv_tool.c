@@ -11,6 +11,9 @@
 int ref_write_extinction_csv(const int64_t*, const int*, int, const char*);
 int ref_write_coexistence_csv(int, int, double, double, int, int64_t, const char*);
 int ref_format_double(double, char*, int);
+int ref_checkpoint_roundtrip(const char*, const char*);
+int ref_output_dir_name(int, int, int, double, int, int, char*, int);
+int ref_write_densities(const int64_t*, const uint64_t*, int, int, const char*, int);
 
 int main(int argc, char** argv) {
     if (argc < 2) return 2;
@@ -27,6 +30,25 @@ int main(int argc, char** argv) {
     if (!strcmp(argv[1], "coexistence") && argc == 9)
         return ref_write_coexistence_csv(atoi(argv[3]), atoi(argv[4]), strtod(argv[5], 0), strtod(argv[6], 0),
                                          atoi(argv[7]), strtoll(argv[8], 0, 10), argv[2]);
+    if (!strcmp(argv[1], "roundtrip") && argc == 4) return ref_checkpoint_roundtrip(argv[2], argv[3]);
+    if (!strcmp(argv[1], "dirname") && argc == 8) {
+        char buf[256];
+        int rc = ref_output_dir_name(atoi(argv[2]), atoi(argv[3]), atoi(argv[4]), strtod(argv[5], 0), atoi(argv[6]),
+                                     atoi(argv[7]), buf, 256);
+        puts(buf);
+        return rc;
+    }
+    if (!strcmp(argv[1], "densities") && argc >= 6) { /* densities <path> <append> <S> mcs c0..cS ... */
+        int append = atoi(argv[3]), S = atoi(argv[4]);
+        int n = (argc - 5) / (S + 2);
+        int64_t* st = malloc(sizeof(int64_t) * (n + 1));
+        uint64_t* c = malloc(sizeof(uint64_t) * (n + 1) * (S + 1));
+        for (int i = 0; i < n; ++i) {
+            st[i] = strtoll(argv[5 + i * (S + 2)], 0, 10);
+            for (int v = 0; v <= S; ++v) c[i * (S + 1) + v] = strtoull(argv[6 + i * (S + 2) + v], 0, 10);
+        }
+        return ref_write_densities(st, c, n, S, argv[2], append);
+    }
     if (!strcmp(argv[1], "format")) {
         char buf[64];
         for (int i = 2; i < argc; ++i) {

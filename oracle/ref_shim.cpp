@@ -6,6 +6,7 @@
 //   (escg_oracle.c), to generate tests/golden/ fixtures, and as the timed CPU baseline
 //   (bench.py --impl reference / cpu_baseline.kind == "reference").
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -274,6 +275,48 @@ EXPORT int ref_write_coexistence_csv(int trials, int coexisting, double probabil
         r.coexisting = coexisting;
         r.probability = probability;
         escg::write_coexistence_csv(r, mobility, length, mcs, path);
+        return 0;
+    } catch (const std::exception& e) {
+        return code_of(e);
+    }
+}
+
+// Checkpoint round trip through the reference (persistence.cpp:322-351): load `src` (written by the
+// device engine), save it again into `dst`.  Used out of process by ref_csv_tool.
+EXPORT int ref_checkpoint_roundtrip(const char* src, const char* dst) {
+    try {
+        auto cp = escg::load_checkpoint(src);
+        escg::save_checkpoint(dst, cp.params, cp.lattice, cp.dominance, cp.saved_mcs);
+        return 0;
+    } catch (const std::exception& e) {
+        fprintf(stderr, "%s\n", e.what());
+        return code_of(e);
+    }
+}
+
+EXPORT int ref_output_dir_name(int length, int height, int n, double mobility, int flux, int species, char* buf,
+                               int cap) {
+    escg::SimParams p;
+    p.length = length;
+    p.height = height;
+    p.neighbourhood = n == 8 ? escg::Neighbourhood::Moore8 : escg::Neighbourhood::VonNeumann4;
+    p.mobility = mobility;
+    p.flux = flux != 0;
+    p.species = species;
+    const std::string s = escg::output_dir_name(p);
+    if (static_cast<int>(s.size()) + 1 > cap) return -1;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+EXPORT int ref_write_densities(const std::int64_t* steps, const std::uint64_t* counts, int n, int species,
+                               const char* path, int append) {
+    try {
+        escg::DensityTrace tr;
+        for (int i = 0; i < n; ++i)
+            tr.append(steps[i], std::vector<std::uint64_t>(counts + static_cast<size_t>(i) * (species + 1),
+                                                          counts + static_cast<size_t>(i + 1) * (species + 1)));
+        escg::export_densities(tr, path, append != 0);
         return 0;
     } catch (const std::exception& e) {
         return code_of(e);
