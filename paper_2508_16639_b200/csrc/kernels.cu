@@ -20,8 +20,10 @@
 namespace escgd {
 
 #ifdef ESCG_DIAG_TIMING
-// diagnostic builds only: per-CTA %globaltimer stamps of the block kernel's sections
+// diagnostic builds only: per-CTA %globaltimer stamps of the block kernel's sections, and per-warp
+// stamps at the end of each phase's work (before the phase barrier) of CTA 0..7
 __device__ unsigned long long g_diag_t[4096 * 16];
+__device__ unsigned long long g_diag_w[8 * 32 * 16];
 #endif
 
 namespace {
@@ -83,32 +85,75 @@ __device__ __forceinline__ int udiv_small(int n, int d) {
     return q;
 }
 
+// Sum of the four bytes of a (each byte <= 255).
+__device__ __forceinline__ uint32_t byte_sum(uint32_t a) {
+    const uint32_t h = (a & 0x00FF00FFu) + ((a >> 8) & 0x00FF00FFu);
+    return (h & 0xFFFFu) + (h >> 16);
+}
+
 // Species histogram of a rows x cols region of a byte array (generic pointer, any space) with the
-// given pitch into sCnt (shared, zeroed by the caller).  Warps take rows, lanes take 4-byte words;
-// S1 <= 8 uses SIMD byte compares + popc in registers.
+// given pitch, added into sCnt[0, S1) (shared; the caller zeroes sCnt[0, kCntSlots) and syncs
+// before, and syncs after).  S1 <= 8: every thread walks 4-byte words of the flattened region and
+// accumulates, per byte lane, the bit-subset indicators b0, b1, b2, b0b1, b0b2, b1b2, b0b1b2 of the
+// cell codes (plain adds, flushed every 255 words); the exact per-code counts follow by inclusion-
+// exclusion.  Otherwise one shared atomic per cell.
 __device__ void block_count(const uint8_t* base, int rows, int cols, int pitch, int S1, uint32_t* sCnt) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     if (S1 <= 8 && (cols & 3) == 0 && (pitch & 3) == 0 && ((reinterpret_cast<uintptr_t>(base) & 3) == 0)) {
-        uint32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        const int wpr = cols >> 2;
-        for (int y = warp; y < rows; y += nw) {
-            const uint32_t* row = reinterpret_cast<const uint32_t*>(base + static_cast<size_t>(y) * pitch);
-            for (int x = lane; x < wpr; x += 32) {
-                const uint32_t w = row[x];
+        const int wpr = cols >> 2, n = rows * wpr;
+        const int nb = S1 <= 2 ? 1 : (S1 <= 4 ? 2 : 3);  // code bits
+        uint32_t s[7] = {0, 0, 0, 0, 0, 0, 0};           // s0 s1 s2 s01 s02 s12 s012
+        uint32_t a[7] = {0, 0, 0, 0, 0, 0, 0};
+        int y = udiv_small(tid, wpr), x = tid - y * wpr;
+        const int dy = udiv_small(nt, wpr), dx = nt - dy * wpr;
+        int pend = 0;
+        for (int k = tid; k < n; k += nt) {
+            const uint32_t w = *reinterpret_cast<const uint32_t*>(base + static_cast<size_t>(y) * pitch + 4 * x);
+            const uint32_t b0 = w & 0x01010101u, b1 = (w >> 1) & 0x01010101u, b2 = (w >> 2) & 0x01010101u;
+            a[0] += b0;
+            if (nb >= 2) {
+                a[1] += b1;
+                a[3] += b0 & b1;
+            }
+            if (nb >= 3) {
+                a[2] += b2;
+                a[4] += b0 & b2;
+                a[5] += b1 & b2;
+                a[6] += b0 & b1 & b2;
+            }
+            if (++pend == 255) {
 #pragma unroll
-                for (int v = 0; v < 8; ++v)
-                    if (v < S1) c[v] += __popc(__vcmpeq4(w, 0x01010101u * static_cast<uint32_t>(v)));
+                for (int i = 0; i < 7; ++i) {
+                    s[i] += byte_sum(a[i]);
+                    a[i] = 0;
+                }
+                pend = 0;
+            }
+            x += dx;
+            y += dy;
+            if (x >= wpr) {
+                x -= wpr;
+                ++y;
             }
         }
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            if (v < S1) {
-                const uint32_t s = __reduce_add_sync(0xffffffffu, c[v]);
-                if (lane == 0 && s) atomicAdd(&sCnt[v], s >> 3);
-            }
+        for (int i = 0; i < 7; ++i) {
+            const uint32_t t = __reduce_add_sync(0xffffffffu, s[i] + byte_sum(a[i]));
+            if (lane == 0 && t) atomicAdd(&sCnt[kMaxSpecies + 1 - 7 + i], t);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t* z = sCnt + kMaxSpecies + 1 - 7;
+            const uint32_t N = static_cast<uint32_t>(rows) * static_cast<uint32_t>(cols);
+            const uint32_t s0 = z[0], s1 = z[1], s2 = z[2], s01 = z[3], s02 = z[4], s12 = z[5], s012 = z[6];
+            const uint32_t c[8] = {N - s0 - s1 - s2 + s01 + s02 + s12 - s012, s0 - s01 - s02 + s012,
+                                   s1 - s01 - s12 + s012, s01 - s012, s2 - s02 - s12 + s012, s02 - s012,
+                                   s12 - s012, s012};
+            for (int v = 0; v < S1; ++v) sCnt[v] += c[v];
+            for (int i = 0; i < 7; ++i) z[i] = 0;
         }
     } else {
-        for (int y = warp; y < rows; y += nw)
+        for (int y = tid >> 5; y < rows; y += nt >> 5)
             for (int x = lane; x < cols; x += 32) atomicAdd(&sCnt[base[static_cast<size_t>(y) * pitch + x]], 1u);
     }
 }
@@ -306,7 +351,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     for (;;) {
         int64_t adv;
         if (a.record) {
-            for (int v = tid; v < S1; v += nt) sCnt[v] = 0;
+            for (int v = tid; v <= kMaxSpecies; v += nt) sCnt[v] = 0;
             __syncthreads();
             block_count(lat + kTileR0 * P + kTileC0, H, L, P, S1, sCnt);
             __syncthreads();
@@ -444,6 +489,16 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
                     w = nw;
                 }
             }
+#ifdef ESCG_DIAG_TIMING
+            {
+                const int cta = blockIdx.x + gridDim.x * blockIdx.y;
+                if (cta < 8 && (threadIdx.x & 31) == 0 && q < 16) {
+                    unsigned long long tw;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw));
+                    g_diag_w[(cta * 32 + (threadIdx.x >> 5)) * 16 + q] = tw;
+                }
+            }
+#endif
 #ifndef ESCG_DIAG_NO_PHASE_SYNC
             __syncthreads();
 #endif
@@ -629,7 +684,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
 #endif
     }
     if (a.count) {
-        for (int v = tid; v < S1; v += nt) sCnt[v] = 0;
+        for (int v = tid; v <= kMaxSpecies; v += nt) sCnt[v] = 0;
         __syncthreads();
         if (a.step)
             block_count(win + My * P + Mx, bh, bw, P, S1, sCnt);
@@ -709,7 +764,7 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
 
     // record_and_check on the current lattice (block region in `src`, pitch `pitch`)
     auto do_record = [&](const uint8_t* base, int pitch) {
-        for (int v = tid; v < S1; v += nt) sCnt[v] = 0;
+        for (int v = tid; v <= kMaxSpecies; v += nt) sCnt[v] = 0;
         __syncthreads();
         block_count(base, bh, bw, pitch, S1, sCnt);
         __syncthreads();
@@ -899,6 +954,19 @@ int tile_smem_bytes(int H, int L, int S, int* pitch) {
 }
 
 // Diagnostic: copy the block kernel's section stamps (ESCG_DIAG_TIMING builds; else returns 0).
+extern "C" __attribute__((visibility("default"))) int escg_diag_warps(unsigned long long* out, int n) {
+#ifdef ESCG_DIAG_TIMING
+    return cudaMemcpyFromSymbol(out, g_diag_w, sizeof(unsigned long long) * (n < 8 * 32 * 16 ? n : 8 * 32 * 16)) ==
+                   cudaSuccess
+               ? n
+               : -1;
+#else
+    (void)out;
+    (void)n;
+    return 0;
+#endif
+}
+
 extern "C" __attribute__((visibility("default"))) int escg_diag_timing(unsigned long long* out, int n) {
 #ifdef ESCG_DIAG_TIMING
     return cudaMemcpyFromSymbol(out, g_diag_t, sizeof(unsigned long long) * (n < 4096 * 16 ? n : 4096 * 16)) ==

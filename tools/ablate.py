@@ -22,8 +22,11 @@ if __name__ == "__main__":
             build(out=os.path.join(ROOT, "tools", "_ablate_%s.so" % name), defines=defs)
         sys.exit(0)
     L = int(sys.argv[1]) if len(sys.argv) > 1 else 3200
+    only = os.environ.get("ABLATE", "")
     for name in VARIANTS:
+        if only and name not in only.split(","):
+            continue
         env = dict(os.environ, ESCG_LIB=os.path.join(ROOT, "tools", "_ablate_%s.so" % name))
-        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "one_block.py"), str(L), "200"],
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "one_block.py"), str(L), "200"] + sys.argv[2:],
                              env=env, capture_output=True, text=True)
         print(name, out.stdout.strip(), out.stderr.strip()[-200:], flush=True)

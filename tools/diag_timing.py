@@ -29,3 +29,18 @@ with e.DeviceEngine(p, e.make_circulant(3, [1]), kernel="block") as eng:
     for s in [0, 1, 2, 3, 4, 5, 6, 8, 9]:
         rel = (t[:, s] - t0) / 1e3
         print("%-12s min %7.2f  median %7.2f  max %7.2f us" % (names[s], rel.min(), np.median(rel), rel.max()))
+    wb = np.zeros(8 * 32 * 16, np.uint64)
+    lib.escg_diag_warps.argtypes = [C.c_void_p, C.c_int]
+    lib.escg_diag_warps(wb.ctypes.data, wb.size)
+    w = wb.reshape(8, 32, 16).astype(np.int64)
+    for c in range(2):
+        base = t[c, 2]  # load_done of that CTA
+        print("CTA %d per-phase warp finish times (us after load): " % c)
+        prev = base
+        for q in range(4 * d["kmcs"]):
+            col = w[c, :, q]
+            if col.max() == 0:
+                break
+            rel = (col - prev) / 1e3
+            print("  phase %d: warp work min %.2f median %.2f max %.2f us" % (q, rel.min(), np.median(rel), rel.max()))
+            prev = col.max()
