@@ -433,7 +433,51 @@ EXPORT void orc_crs_round(uint64_t seed, uint64_t mcs, int* oy, int* ox, int* pe
     for (int k = 0; k < 4; ++k) perm[k] = kPerm[pi][k];
 }
 
-static int crs_tiles(int n, int o, int periodic) { return periodic ? n / 2 : (n + o + 1) / 2; }
+static int crs_tiles(int n, int o, int periodic) {
+    if (periodic) return (n % 4 == 0) ? n / 2 : (n + 1) / 2;
+    return (n + o + 1) / 2;
+}
+
+/* Periodic axis of length n >= 4.  n % 4 == 0: T = n/2 tiles, colours t & 1.
+ * Otherwise T = ceil(n/2) tiles (the last one holds one cell when n is odd) and one seam tile takes
+ * a third colour: the tile ring then has odd length (n % 4 in {1, 2}: seam = T-1) or, for n % 4 == 3,
+ * a chord between tiles T-2 and 0 (their footprints meet across the 1-cell tile; seam = T-2).
+ * Returns the number of colours; *seam = seam tile (or -1). */
+static int crs_axis(int n, int* seam) {
+    const int T = (n + 1) / 2;
+    if (n % 4 == 0) {
+        *seam = -1;
+        return 2;
+    }
+    *seam = (n % 4 == 3) ? T - 2 : T - 1;
+    return 3;
+}
+
+static int crs_colour(int t, int seam) { return t == seam ? 2 : (t & 1); }
+
+/* Phase order of an MCS for cy x cx colours.  4 colours: the lexicographic permutation table of
+ * orc_crs_round (unchanged).  6 or 9: Fisher-Yates over colour ids v = cy * ncx + cx driven by the
+ * 16-bit halves of a second ROUND draw (attempt field 1): j = (half_k * (i + 1)) >> 16 for
+ * i = np-1 .. 1, k = np-1-i. */
+EXPORT void orc_crs_round_g(uint64_t seed, uint64_t mcs, int ncy, int ncx, int* oy, int* ox, int* perm) {
+    int p4[4];
+    orc_crs_round(seed, mcs, oy, ox, p4);
+    const int np = ncy * ncx;
+    if (np == 4) {
+        for (int k = 0; k < 4; ++k) perm[k] = p4[k];
+        return;
+    }
+    uint32_t w[4];
+    crs_draw(seed, 0u, mcs, DOM_ROUND, 0, 1, w);
+    for (int k = 0; k < np; ++k) perm[k] = k;
+    for (int i = np - 1, k = 0; i >= 1; --i, ++k) {
+        const uint32_t half = (w[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+        const int j = (int)((half * (uint32_t)(i + 1)) >> 16);
+        const int t = perm[i];
+        perm[i] = perm[j];
+        perm[j] = t;
+    }
+}
 
 /* Device init_lattice (the device counterpart of lattice.hpp:53-66): the same transformation of
  * two uniform words per cell (empty test via next_unit, species via % S + 1), drawn from the
@@ -485,17 +529,22 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
     const int periodic = flux != 0;
     const int db = arity == 8 ? 3 : 2;
     const int lb = db + 2;
-    if (periodic && ((length % 4) != 0 || (height % 4) != 0)) return 2;
+    if (periodic && (length < 4 || height < 4)) return 2;
+    int seam_y = -1, seam_x = -1;
+    const int ncy = periodic ? crs_axis(height, &seam_y) : 2, ncx = periodic ? crs_axis(length, &seam_x) : 2;
+    if (narrow && (ncy != 2 || ncx != 2 || length % 8 != 0)) return 2;
     orc_ctx_make(&c, length, height, species, arity, flux, dom, mobility);
     for (int64_t mcs = mcs0; mcs < mcs0 + n_mcs; ++mcs) {
-        int oy, ox, perm[4];
-        orc_crs_round(seed, (uint64_t)mcs, &oy, &ox, perm);
+        int oy, ox, perm[9];
+        orc_crs_round_g(seed, (uint64_t)mcs, ncy, ncx, &oy, &ox, perm);
         const int ty_n = crs_tiles(height, oy, periodic), tx_n = crs_tiles(length, ox, periodic);
         const int tq = (tx_n + 3) / 4;
-        for (int p = 0; p < 4; ++p) {
-            const int cy = perm[p] >> 1, cx = perm[p] & 1;
-            for (int ty = cy; ty < ty_n; ty += 2) {
-                for (int tx = cx; tx < tx_n; tx += 2) {
+        for (int p = 0; p < ncy * ncx; ++p) {
+            const int cy = perm[p] / ncx, cx = perm[p] % ncx;
+            for (int ty = 0; ty < ty_n; ++ty) {
+                if ((periodic ? crs_colour(ty, seam_y) : (ty & 1)) != cy) continue;
+                for (int tx = 0; tx < tx_n; ++tx) {
+                    if ((periodic ? crs_colour(tx, seam_x) : (tx & 1)) != cx) continue;
                     const uint32_t tile = (uint32_t)ty * (uint32_t)tx_n + (uint32_t)tx;
                     const uint32_t sid = narrow ? (uint32_t)ty * (uint32_t)tq + (uint32_t)(tx >> 2) : tile;
                     const int h = (tx >> 1) & 1;
@@ -511,6 +560,8 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
                         const uint32_t x = (hi_part << hi_shift) | (rf[0] & ((1u << hi_shift) - 1u));
                         int y = 2 * ty - oy + dy, xc = 2 * tx - ox + dx;
                         if (periodic) {
+                            /* the missing half of an odd axis' last tile: no attempt */
+                            if (2 * ty + dy >= height || 2 * tx + dx >= length) continue;
                             y = (y + height) % height;
                             xc = (xc + length) % length;
                         } else if (y < 0 || y >= height || xc < 0 || xc >= length) {

@@ -85,6 +85,8 @@ class Oracle:
         L.orc_philox.argtypes = [_u32, _u32, _u32]
         L.orc_crs_round.argtypes = [C.c_uint64, C.c_uint64, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                     _p(dtype=np.intc, flags="C_CONTIGUOUS")]
+        L.orc_crs_round_g.argtypes = [C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), _p(dtype=np.intc, flags="C_CONTIGUOUS")]
         L.orc_crs_init.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint64, _i32]
         L.orc_crs_run.restype = C.c_int
         L.orc_crs_run.argtypes = [_i32, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _f64, C.c_double, C.c_uint64,
@@ -165,6 +167,12 @@ class Oracle:
         perm = np.zeros(4, np.intc)
         self.lib.orc_crs_round(seed, mcs, C.byref(oy), C.byref(ox), perm)
         return oy.value, ox.value, perm.tolist()
+
+    def crs_round_g(self, seed, mcs, ncy, ncx):
+        oy, ox = C.c_int(0), C.c_int(0)
+        perm = np.zeros(9, np.intc)
+        self.lib.orc_crs_round_g(seed, mcs, ncy, ncx, C.byref(oy), C.byref(ox), perm)
+        return oy.value, ox.value, perm[:ncy * ncx].tolist()
 
     def crs_init(self, length, height, species, empty_prob, seed):
         cells = np.zeros(length * height, np.int32)

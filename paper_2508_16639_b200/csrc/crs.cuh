@@ -78,6 +78,56 @@ __device__ __forceinline__ Round round_params(uint32_t s32, uint64_t mcs) {
     return r;
 }
 
+// Phase order for ncy x ncx colours (escg_oracle.c orc_crs_round_g): colour id of
+// phase p in nibble p.  Four colours use round_params' table; 6 or 9 a Fisher-Yates shuffle driven by
+// the 16-bit halves of a second ROUND draw (attempt field 1).
+struct RoundG {
+    int oy, ox;
+    uint64_t order;
+    __device__ __forceinline__ int colour(int p) const { return static_cast<int>((order >> (4 * p)) & 15u); }
+};
+
+__device__ __forceinline__ RoundG round_params_g(uint32_t s32, uint64_t mcs, int ncy, int ncx) {
+    const Round r4 = round_params(s32, mcs);
+    RoundG r;
+    r.oy = r4.oy;
+    r.ox = r4.ox;
+    const int np = ncy * ncx;
+    if (np == 4) {
+        r.order = 0;
+        for (int p = 0; p < 4; ++p) r.order |= static_cast<uint64_t>(r4.colour(p)) << (4 * p);
+        return r;
+    }
+    const uint4 w = philox(0u, static_cast<uint32_t>(mcs), ctr2(mcs, kDomRound, 0u, 1u), s32);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    uint64_t ord = 0x876543210ull;
+    for (int i = np - 1, k = 0; i >= 1; --i, ++k) {
+        const uint32_t half = (ws[k >> 1] >> (16 * (k & 1))) & 0xFFFFu;
+        const int j = static_cast<int>((half * static_cast<uint32_t>(i + 1)) >> 16);
+        const uint64_t vi = (ord >> (4 * i)) & 15u, vj = (ord >> (4 * j)) & 15u;
+        ord &= ~((15ull << (4 * i)) | (15ull << (4 * j)));
+        ord |= (vi << (4 * j)) | (vj << (4 * i));
+    }
+    r.order = ord;
+    return r;
+}
+
+// Periodic axis of length n >= 4: tiles T, colours (2 or 3), seam tile (-1 if none).
+struct SeamAxis {
+    int T, nc, seam;
+    __host__ __device__ SeamAxis(int n) {
+        T = (n % 4 == 0) ? n / 2 : (n + 1) / 2;
+        nc = (n % 4 == 0) ? 2 : 3;
+        seam = (n % 4 == 0) ? -1 : ((n % 4 == 3) ? T - 2 : T - 1);
+    }
+    // tiles of colour c: c < 2 → t = c + 2i (i < count), c == 2 → the seam tile
+    __device__ __forceinline__ int count(int c) const {
+        if (c == 2) return 1;
+        return ((T - c + 1) >> 1) - ((seam >= 0 && (seam & 1) == c) ? 1 : 0);
+    }
+    __device__ __forceinline__ int tile(int c, int i) const { return c == 2 ? seam : c + 2 * i; }
+};
+
 // (drow, dcol) of direction d (params.hpp:81: up, down, left, right, ul, ur, dl, dr).
 __host__ __device__ __forceinline__ void dir_rc(uint32_t d, int& dr, int& dc) {
     dr = (d < 4u) ? ((d < 2u) ? ((d & 1u) ? 1 : -1) : 0) : ((d & 2u) ? 1 : -1);
@@ -371,6 +421,21 @@ __device__ __forceinline__ void pair_wide(const uint4 wA, uint32_t baseA, uint32
     const uint32_t bA[4] = {wA.x, wA.y, wA.z, wA.w};
     const uint32_t bB[4] = {wB.x, wB.y, wB.z, wB.w};
     tile_dual<ARITY, false>(bA, baseA, tA, bB, baseB, tB, C);
+}
+
+// Seam variant (periodic axes of any length >= 4, WIDE format): the missing half of an odd axis'
+// last tile (part_y / part_x) takes no attempt; everything else is the periodic attempt.
+template <int ARITY>
+__device__ __forceinline__ void tile_seam(const uint4 w, uint32_t base, uint32_t tile, bool part_y, bool part_x,
+                                          const PhaseCtx& C) {
+    constexpr int DB = Bits<ARITY>::DB;
+    const uint32_t words[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const uint32_t word = words[a];
+        if ((part_y && ((word >> DB) & 1u)) || (part_x && ((word >> (DB + 1)) & 1u))) continue;
+        attempt<ARITY, false>(word, base, tile, a, C);
+    }
 }
 
 // Mirror-reflect variant (flux=false, lattice.hpp:42-47; WIDE format only): tile cells outside the

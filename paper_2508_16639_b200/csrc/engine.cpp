@@ -708,24 +708,27 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         int tpitch = 0;
         const int tbytes = escgd::tile_smem_bytes(h->H, h->L, species, &tpitch);
         const bool periodic4 = h->flux && (h->H % 4 == 0) && (h->L % 4 == 0);
-        if (h->flux && !periodic4)
-            config_error("device engine: periodic lattices need L and H divisible by 4 (2x2 tiles, 2 colours per axis)");
+        if (h->flux && (h->H < 4 || h->L < 4))
+            config_error("device engine: periodic lattices need L, H >= 4 (2x2 tiles, footprints may not wrap)");
         int choice = kernel;
         if (choice == ESCG_KERNEL_AUTO) choice = tbytes <= smem_cap ? ESCG_KERNEL_TILE : ESCG_KERNEL_BLOCK;
         if (choice == ESCG_KERNEL_TILE && tbytes > smem_cap)
             config_error("lattice too large for the shared-memory tile kernel");
-        if (choice == ESCG_KERNEL_BLOCK && !periodic4)
+        if (choice == ESCG_KERNEL_BLOCK && !h->flux)
             config_error("block kernel supports periodic (flux) lattices only");
+        if (choice == ESCG_KERNEL_BLOCK && !periodic4)
+            config_error("block kernel needs L and H divisible by 4 (lattices with seams run on the tile kernel, "
+                         "which holds them up to its shared-memory size)");
         h->kernel = choice;
         // NARROW (16-bit attempt words, one draw per tile pair) when migrations dominate so much that
         // at most 1/64 of attempts leave the coarse fast path; needs periodic wrap and L % 8 == 0.
         {
             const int LB = h->arity == 8 ? 5 : 4, CB = 16 - LB;
             const uint64_t fast_coarse = h->th.xm >> (32 - CB);
-            h->narrow = (h->flux && h->L % 8 == 0 && fast_coarse * 64 >= 63ull * (1ull << CB)) ? 1 : 0;
+            h->narrow = (periodic4 && h->L % 8 == 0 && fast_coarse * 64 >= 63ull * (1ull << CB)) ? 1 : 0;
             if (const char* f = std::getenv("ESCG_DRAW_FORMAT")) {
                 if (std::strcmp(f, "wide") == 0) h->narrow = 0;
-                if (std::strcmp(f, "narrow") == 0 && h->flux && h->L % 8 == 0) h->narrow = 1;
+                if (std::strcmp(f, "narrow") == 0 && periodic4 && h->L % 8 == 0) h->narrow = 1;
             }
         }
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));

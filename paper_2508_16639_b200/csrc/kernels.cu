@@ -227,11 +227,49 @@ __device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, 
     return C;
 }
 
+// Tile-kernel lattice modes: periodic with H, L ≡ 0 (mod 4); reflecting; periodic with seams.
+constexpr int kModePeriodic = 0, kModeReflect = 1, kModeSeam = 2;
+
+// One MCS of the seam mode: 4, 6 or 9 phases of single WIDE tiles.
+template <int ARITY>
+__device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t tbl, uint32_t sT,
+                                const RuleArgs& rule, int H, int L, int P, int S1, uint32_t s32, uint64_t mcs) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const SeamAxis ay(H), ax(L);
+    const RoundG rg = round_params_g(s32, mcs, ay.nc, ax.nc);
+    const int np = ay.nc * ax.nc;
+#pragma unroll 1
+    for (int p = 0; p < np; ++p) {
+        const int v = rg.colour(p), cy = v / ax.nc, cx = v - cy * ax.nc;
+        const PhaseCtx C = phase_ctx<ARITY>(rule, 0, tbl, sT, S1, mcs, p, s32);
+        const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+        const int nty = ay.count(cy), ntx = ax.count(cx), cnt = nty * ntx;
+        for (int k = tid; k < cnt; k += nt) {
+            const int i = k / ntx, j = k - i * ntx;
+            const int ty = ay.tile(cy, i), tx = ax.tile(cx, j);
+            const uint32_t tile = static_cast<uint32_t>(ty) * static_cast<uint32_t>(ax.T) + static_cast<uint32_t>(tx);
+            const uint32_t base =
+                lat0 + static_cast<uint32_t>((2 * ty - rg.oy + kTileR0) * P + kTileC0 + 2 * tx - rg.ox);
+            tile_seam<ARITY>(philox(tile, C.c1, c2, s32), base, tile, 2 * ty + 1 >= H, 2 * tx + 1 >= L, C);
+        }
+        __syncthreads();
+        ghost_pass<true>(lat, snap, H, L, P);
+        __syncthreads();
+        ghost_pass<false>(lat, snap, H, L, P);
+        __syncthreads();
+    }
+}
+
 // One MCS of the tile kernel (whole lattice in shared memory at lat0, ghost frame when periodic).
-template <int ARITY, bool REFLECT>
+template <int ARITY, int MODE>
 __device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t tbl, uint32_t sT,
                            const RuleArgs& rule, int narrow, int H, int L, int P, int S1, uint32_t s32,
                            uint64_t mcs) {
+    if (MODE == kModeSeam) {
+        tile_round_seam<ARITY>(lat0, lat, snap, tbl, sT, rule, H, L, P, S1, s32, mcs);
+        return;
+    }
+    constexpr bool REFLECT = MODE == kModeReflect;
     const int tid = threadIdx.x, nt = blockDim.x;
     const Round rp = round_params(s32, mcs);
     const int Ty = REFLECT ? (H + rp.oy + 1) >> 1 : H >> 1;
@@ -321,8 +359,9 @@ __device__ void tile_copy(uint8_t* lat, uint8_t* glat, int H, int L, int P) {
     }
 }
 
-template <int ARITY, bool REFLECT>
+template <int ARITY, int MODE>
 __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
+    constexpr bool REFLECT = MODE == kModeReflect;
     extern __shared__ __align__(16) uint8_t smem[];
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
     const TileSmem lay = tile_layout(H, L, a.S, P);
@@ -369,7 +408,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
             adv = a.run.mcs_limit - mcs;
         }
         for (int64_t k = 0; k < adv; ++k, ++mcs)
-            tile_round<ARITY, REFLECT>(lat0, lat, snap, tbl, sTa, a.rule, a.narrow, H, L, P, S1, s32,
+            tile_round<ARITY, MODE>(lat0, lat, snap, tbl, sTa, a.rule, a.narrow, H, L, P, S1, s32,
                                        static_cast<uint64_t>(mcs));
     }
     tile_copy<false>(lat, glat, H, L, P);
@@ -998,9 +1037,9 @@ cudaError_t launch_count(const uint8_t* lat, int64_t n, int nrep, int S, unsigne
     return cudaGetLastError();
 }
 
-template <int ARITY, bool REFLECT>
+template <int ARITY, int MODE>
 static cudaError_t tile_launch_t(const TileArgs& a, int nrep, int threads, cudaStream_t s) {
-    auto k = tile_kernel<ARITY, REFLECT>;
+    auto k = tile_kernel<ARITY, MODE>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<nrep, threads, a.smem_bytes, s>>>(a);
@@ -1008,8 +1047,15 @@ static cudaError_t tile_launch_t(const TileArgs& a, int nrep, int threads, cudaS
 }
 
 cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s) {
-    if (a.arity == 8) return a.flux ? tile_launch_t<8, false>(a, nrep, threads, s) : tile_launch_t<8, true>(a, nrep, threads, s);
-    return a.flux ? tile_launch_t<4, false>(a, nrep, threads, s) : tile_launch_t<4, true>(a, nrep, threads, s);
+    const int mode = !a.flux ? kModeReflect : ((a.H % 4 == 0 && a.L % 4 == 0) ? kModePeriodic : kModeSeam);
+    if (a.arity == 8) {
+        if (mode == kModeReflect) return tile_launch_t<8, kModeReflect>(a, nrep, threads, s);
+        if (mode == kModeSeam) return tile_launch_t<8, kModeSeam>(a, nrep, threads, s);
+        return tile_launch_t<8, kModePeriodic>(a, nrep, threads, s);
+    }
+    if (mode == kModeReflect) return tile_launch_t<4, kModeReflect>(a, nrep, threads, s);
+    if (mode == kModeSeam) return tile_launch_t<4, kModeSeam>(a, nrep, threads, s);
+    return tile_launch_t<4, kModePeriodic>(a, nrep, threads, s);
 }
 
 template <int ARITY>

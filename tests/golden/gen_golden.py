@@ -191,6 +191,25 @@ def _traj(args):
     return [res["counts"][i].tolist() for i in idx], res["steps"][idx].tolist()
 
 
+def _traj_lh(args):
+    L, H, M, p0, mcs, seed, every = args
+    r = ref()
+    res = r.simulate(L, H, r.circulant(3, [1]), M, p0, mcs, seed, mode=0, want_cells=False)
+    idx = list(range(0, len(res["steps"]), every))
+    return [res["counts"][i].tolist() for i in idx], res["steps"][idx].tolist()
+
+
+def gen_stats_seam(out):
+    """Ensembles on periodic lattices whose sides are not divisible by 4 (device seam schedule)."""
+    with Pool(8) as pool:
+        for (L, H) in [(50, 50), (51, 45)]:
+            tr = pool.map(_traj_lh, [(L, H, 1e-3, 0.1, 300, 4000 + s, 50) for s in range(64)])
+            out["rps_L%dx%d_traj" % (L, H)] = {
+                "desc": "RPS %dx%d periodic M=1e-3 p0=0.1: counts every 50 MCS to 300" % (L, H),
+                "counts": [t[0] for t in tr], "steps": tr[0][1]}
+    return out
+
+
 def _park(seed):
     r = ref()
     res = r.simulate(100, 100, r.park8(0.15, 0.75, 1.0), 0.0, 0.0, 1000, seed, mode=0, want_cells=False)
@@ -231,4 +250,6 @@ if __name__ == "__main__":
     dump("serial.json", gen_serial())
     dump("rule.json", gen_rule())
     if "--stats" in sys.argv:
-        dump("stats.json", gen_stats())
+        dump("stats.json", gen_stats_seam(gen_stats()))
+    elif "--stats-seam" in sys.argv:
+        dump("stats.json", gen_stats_seam(json.load(open(os.path.join(HERE, "stats.json")))))

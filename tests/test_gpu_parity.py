@@ -100,6 +100,13 @@ CRS_CASES = [
     (30, 22, 8, 0.0, 0.0, 4, False, "park8"),
     (21, 35, 3, 1e-3, 0.1, 8, False, "rps"),
     (13, 6, 3, 1e-2, 0.3, 4, False, "rps"),
+    # periodic lattices with seams (L or H not divisible by 4: 6 or 9 colour phases)
+    (50, 50, 3, 3e-5, 0.1, 4, True, "rps"),
+    (21, 15, 3, 1e-3, 0.1, 8, True, "rps"),
+    (7, 6, 5, 1e-2, 0.0, 4, True, "rpsls"),
+    (102, 33, 3, 1e-4, 0.1, 4, True, "rps"),
+    (4, 5, 3, 1e-2, 0.2, 8, True, "rps"),
+    (13, 40, 8, 0.0, 0.0, 4, True, "park8"),
 ]
 
 
@@ -354,3 +361,29 @@ def test_band_group_resume_from_host_lattice(escg):
         grp.set_lattice(start, mcs=40)
         grp.advance(6)
         assert np.array_equal(grp.get_lattice(), single)
+
+
+@pytest.mark.gpu
+def test_seam_lattice_ensemble_matches_oracle(escg, oracle):
+    """Replicas of a seam lattice (odd size) on the tile kernel = independent oracle runs."""
+    L, H, S = 31, 29, 3
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, H, S, 1e-3, 0.1, 4, True, seed=5)
+    with escg.DeviceEngine(p, model, n_replicas=6, seeds=range(50, 56)) as eng:
+        assert eng.describe()["kernel"] == "tile"
+        eng.init_lattice()
+        init = [eng.get_lattice(r) for r in range(6)]
+        eng.advance(9)
+        for r in range(6):
+            want = oracle.crs_run(init[r], L, H, model.matrix(), 1e-3, 50 + r, 0, 9)
+            assert np.array_equal(eng.get_lattice(r), want)
+
+
+@pytest.mark.gpu
+def test_seam_lattices_reject_block_kernel(escg):
+    p = params(escg, 1002, 1000, 3, 1e-4, 0.1, 4, True)
+    with pytest.raises(escg.ConfigError, match="divisible by 4"):
+        escg.DeviceEngine(p, escg.make_circulant(3, [1]), kernel="block")
+    p = params(escg, 3, 8, 3, 1e-4, 0.1, 4, True)
+    with pytest.raises(escg.ConfigError, match=">= 4"):
+        escg.DeviceEngine(p, escg.make_circulant(3, [1]))

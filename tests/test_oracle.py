@@ -194,6 +194,60 @@ def test_crs_tiles_are_disjoint():
                                         seen[key] = (ty, tx)
 
 
+def _axis_colours(n):
+    """tiles and colours of a periodic axis (mirror of escg_oracle.c crs_axis)."""
+    T = n // 2 if n % 4 == 0 else (n + 1) // 2
+    seam = -1 if n % 4 == 0 else (T - 2 if n % 4 == 3 else T - 1)
+    return T, [2 if t == seam else (t & 1) for t in range(T)]
+
+
+@pytest.mark.parametrize("n", list(range(4, 41)) + [50, 101, 102, 103, 200])
+def test_seam_colouring_gives_disjoint_footprints(n):
+    """Periodic axes of any length >= 4: same-colour tiles have disjoint 1-D footprints (their cells
+    +-1, modulo n) for both tiling origins, footprints never wrap onto themselves, and every cell
+    belongs to exactly one tile.  The 2-D (von Neumann / Moore) footprint is the product of the two
+    axes' footprints, so the 2-D colour classes (cy, cx) are disjoint too."""
+    T, col = _axis_colours(n)
+    for o in (0, 1):
+        owner = {}
+        foot = []
+        for t in range(T):
+            cells = [(2 * t + d - o) % n for d in (0, 1) if 2 * t + d < n]
+            for c in cells:
+                assert c not in owner
+                owner[c] = t
+            f = {(c + e) % n for c in cells for e in (-1, 0, 1)}
+            assert len(f) == len(cells) + 2
+            foot.append(f)
+        assert len(owner) == n
+        for t in range(T):
+            for u in range(t + 1, T):
+                if col[t] == col[u]:
+                    assert not (foot[t] & foot[u]), (n, o, t, u)
+
+
+def test_crs_round_generic_permutations(oracle):
+    for ncy, ncx in [(2, 2), (2, 3), (3, 2), (3, 3)]:
+        seen = set()
+        for m in range(200):
+            oy, ox, perm = oracle.crs_round_g(11, m, ncy, ncx)
+            assert sorted(perm) == list(range(ncy * ncx))
+            seen.add(tuple(perm))
+            if ncy * ncx == 4:
+                assert (oy, ox, perm) == oracle.crs_round(11, m)
+        assert len(seen) > (10 if ncy * ncx == 4 else 50)
+
+
+@pytest.mark.parametrize("L,H,arity", [(50, 50, 4), (21, 15, 4), (7, 6, 8), (13, 20, 8), (4, 5, 4)])
+def test_crs_seam_schedule_invariants(oracle, L, H, arity):
+    D = model(oracle, "rps")
+    init = oracle.crs_init(L, H, 3, 0.1, 8)
+    a = oracle.crs_run(init, L, H, D, 1e-2, 8, 0, 12, arity=arity)
+    b = oracle.crs_run(oracle.crs_run(init, L, H, D, 1e-2, 8, 0, 5, arity=arity), L, H, D, 1e-2, 8, 5, 7, arity=arity)
+    assert np.array_equal(a, b)
+    assert a.min() >= 0 and a.max() <= 3 and not np.array_equal(a, init)
+
+
 def test_oracle_matches_compiled_reference(oracle, ref):
     """Direct cross-check with the reference library (only where oracle/_ref was built)."""
     D = ref.circulant(3, [1])
