@@ -66,15 +66,16 @@ struct Round {
 };
 
 __device__ __forceinline__ Round round_params(uint32_t s32, uint64_t mcs) {
-    // Lexicographic permutations of {0,1,2,3}, packed 2 bits per colour (phase 0 in bits 0-1).
-    constexpr uint8_t kPerm[24] = {0xE4, 0xB4, 0xD8, 0x78, 0x9C, 0x6C, 0xE1, 0xB1, 0xC9, 0x39, 0x8D, 0x2D,
-                                   0xD2, 0x72, 0xC6, 0x36, 0x4E, 0x1E, 0x93, 0x63, 0x87, 0x27, 0x4B, 0x1B};
+    // Lexicographic permutations of {0,1,2,3}, packed 2 bits per colour (phase 0 in bits 0-1), one
+    // byte per permutation in three 64-bit immediates (no local-memory table):
+    // E4 B4 D8 78 9C 6C E1 B1 | C9 39 8D 2D D2 72 C6 36 | 4E 1E 93 63 87 27 4B 1B.
     const uint4 w = philox(0u, static_cast<uint32_t>(mcs), ctr2(mcs, kDomRound, 0u, 0u), s32);
     Round r;
     r.oy = static_cast<int>(w.x & 1u);
     r.ox = static_cast<int>((w.x >> 1) & 1u);
     const uint32_t pi = static_cast<uint32_t>((static_cast<uint64_t>(w.y) * 24u) >> 32);
-    r.order = kPerm[pi];
+    const uint64_t K = pi < 8u ? 0xB1E16C9C78D8B4E4ull : (pi < 16u ? 0x36C672D22D8D39C9ull : 0x1B4B278763931E4Eull);
+    r.order = static_cast<uint32_t>((K >> (8u * (pi & 7u))) & 0xFFu);
     return r;
 }
 

@@ -473,59 +473,76 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
                 u0 = 0;
                 nu = (ni + 1) >> 1;
             }
-            const int cnt = nj * nu;
-            if (tid < cnt) {
-                const int q0 = udiv_small(tid, nu), qn = udiv_small(nt, nu);
-                int aa = q0, bb = tid - q0 * nu;
-                const int da = qn, db = nt - qn * nu;
-                // item geometry + draw of item (aa, bb); the draw of the next item is computed
-                // before the current item's attempts (software pipelining of the Philox latency)
-                auto geom = [&](int a_, int b_, uint32_t& bA, uint32_t& bB, uint32_t& tA, uint32_t& tB, uint4& w) {
-                    const int j = j0 + 2 * a_;
-                    const int ty = wrap_down(jb + j, Ty, big);
-                    const uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
-                    const uint32_t trow = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx);
-                    int ia;
+            // Thread -> items: a fixed item column b (pair b of every active tile row) and rows
+            // a0, a0 + R, a0 + 2R, ... with R = floor(threads / nu): the column geometry, the
+            // half-warp chain order and the scratch redirection are per-phase constants, and a row
+            // step is a few adds.  (Items are the same as any other enumeration; order within a
+            // phase is immaterial.)
+            if (nu > 0 && nj > 0) {
+                const int R = udiv_small(nt, nu);
+                const int a0 = udiv_small(tid, nu), b = tid - a0 * nu;
+                if (a0 < R && a0 < nj) {
+                    // upper half-warp runs its pair's second tile as chain 1 (bank split, tile_dual)
+                    const bool sw = (tid & 16) != 0;
+                    int ia1, ia2;  // window tile columns of chain 1 / chain 2
+                    uint32_t tc1, tc2;  // global tile-column part of the tile ids
+                    uint32_t ctrcol = 0;  // NARROW: pair column of the draw counter
                     if (NARROW) {
-                        const int u = u0 + b_;
-                        const int qq = wrap_down((ib >> 2) + u, TQ, big);
-                        w = philox(static_cast<uint32_t>(ty) * static_cast<uint32_t>(TQ) + qq, C.c1, c2, s32);
-                        ia = cx + 4 * u;
-                        tA = trow + 4 * qq + cx;
-                        tB = tA + 2;
+                        const int u = u0 + b;
+                        const int qq = big ? ((ib >> 2) + u) % TQ : wrap_down((ib >> 2) + u, TQ, false);
+                        const int ia = cx + 4 * u;
+                        ctrcol = static_cast<uint32_t>(qq);
+                        ia1 = sw ? ia + 2 : ia;
+                        ia2 = sw ? ia : ia + 2;
+                        tc1 = static_cast<uint32_t>(4 * qq + cx + (sw ? 2 : 0));
+                        tc2 = static_cast<uint32_t>(4 * qq + cx + (sw ? 0 : 2));
                     } else {
-                        ia = i0 + 4 * b_;
-                        tA = trow + wrap_down(ib + ia, Tx, big);
-                        tB = trow + wrap_down(ib + ia + 2, Tx, big);
-                        w = philox(tA, C.c1, c2, s32);
+                        const int ia = i0 + 4 * b;
+                        const uint32_t tA = static_cast<uint32_t>(big ? (ib + ia) % Tx : wrap_down(ib + ia, Tx, false));
+                        const uint32_t tB =
+                            static_cast<uint32_t>(big ? (ib + ia + 2) % Tx : wrap_down(ib + ia + 2, Tx, false));
+                        ia1 = sw ? ia + 2 : ia;
+                        ia2 = sw ? ia : ia + 2;
+                        tc1 = sw ? tB : tA;
+                        tc2 = sw ? tA : tB;
                     }
-                    const bool okA = ia >= imin && ia <= imax, okB = ia + 2 >= imin && ia + 2 <= imax;
-                    bA = okA ? rowbase + 2 * ia : g.scratch;
-                    bB = okB ? rowbase + 2 * ia + 4 : g.scratch + 8;
-                };
-                uint32_t bA, bB, tA, tB;
-                uint4 w;
-                geom(aa, bb, bA, bB, tA, tB, w);
-                for (int k = tid; k < cnt; k += nt) {
-                    bb += db;
-                    aa += da;
-                    if (bb >= nu) {
-                        bb -= nu;
-                        ++aa;
+                    const bool ok1 = ia1 >= imin && ia1 <= imax, ok2 = ia2 >= imin && ia2 <= imax;
+                    const uint32_t scr1 = sw ? g.scratch + 8 : g.scratch, scr2 = sw ? g.scratch : g.scratch + 8;
+                    int j = j0 + 2 * a0;
+                    int ty = (jb + j) % Ty;
+                    const int dTy = (2 * R) % Ty;
+                    uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
+                    const uint32_t dRow = static_cast<uint32_t>(4 * R * P);
+                    auto draw1 = [&](int ty_) {
+                        return NARROW ? philox(static_cast<uint32_t>(ty_) * static_cast<uint32_t>(TQ) + ctrcol, C.c1, c2, s32)
+                                      : philox(static_cast<uint32_t>(ty_) * static_cast<uint32_t>(Tx) + tc1, C.c1, c2, s32);
+                    };
+                    uint4 w = draw1(ty);
+                    for (int a = a0; a < nj; a += R) {
+                        int nty = ty + dTy;
+                        nty = nty >= Ty ? nty - Ty : nty;
+                        uint4 nw = make_uint4(0, 0, 0, 0);
+                        if (a + R < nj) nw = draw1(nty);
+                        const uint32_t trow = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx);
+                        const uint32_t base1 = ok1 ? rowbase + 2 * ia1 : scr1;
+                        const uint32_t base2 = ok2 ? rowbase + 2 * ia2 : scr2;
+                        if (NARROW) {
+                            // pair draw: words (x, y) belong to the pair's first tile, (z, w) to its second
+                            const uint32_t p0 = sw ? w.z : w.x, p1 = sw ? w.w : w.y;
+                            const uint32_t q0 = sw ? w.x : w.z, q1 = sw ? w.y : w.w;
+                            const uint32_t b1[4] = {p0 & 0xFFFFu, p0 >> 16, p1 & 0xFFFFu, p1 >> 16};
+                            const uint32_t b2[4] = {q0 & 0xFFFFu, q0 >> 16, q1 & 0xFFFFu, q1 >> 16};
+                            tile_dual_ordered<ARITY, true>(b1, base1, trow + tc1, b2, base2, trow + tc2, C);
+                        } else {
+                            const uint4 w2 = philox(trow + tc2, C.c1, c2, s32);
+                            const uint32_t b1[4] = {w.x, w.y, w.z, w.w};
+                            const uint32_t b2[4] = {w2.x, w2.y, w2.z, w2.w};
+                            tile_dual_ordered<ARITY, false>(b1, base1, trow + tc1, b2, base2, trow + tc2, C);
+                        }
+                        ty = nty;
+                        rowbase += dRow;
+                        w = nw;
                     }
-                    uint32_t nA = 0, nB = 0, ntA = 0, ntB = 0;
-                    uint4 nw = make_uint4(0, 0, 0, 0);
-                    if (k + nt < cnt) geom(aa, bb, nA, nB, ntA, ntB, nw);
-                    if (NARROW) {
-                        pair_narrow<ARITY>(w, bA, tA, bB, tB, C);
-                    } else {
-                        pair_wide<ARITY>(w, bA, tA, philox(tB, C.c1, c2, s32), bB, tB, C);
-                    }
-                    bA = nA;
-                    bB = nB;
-                    tA = ntA;
-                    tB = ntB;
-                    w = nw;
                 }
             }
 #ifdef ESCG_DIAG_TIMING
