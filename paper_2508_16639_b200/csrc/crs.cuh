@@ -159,29 +159,45 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// Offset table: entry (dir | dy << DB | dx << DB+1) = (cell offset, neighbour offset) from the
-// tile's (0,0) cell in a row-major window of pitch P.
+// Per-CTA state of the attempt paths in static shared memory (immediate addresses, no registers):
+//   sOffTbl  entry (dir | dy << DB | dx << DB+1) = (cell offset, neighbour offset) from the tile's
+//            (0,0) cell in a row-major window of pitch P;
+//   sSlow    what only the exact (slow) paths and the WIDE rule read: X_mig, X_int, the smem
+//            address of the (S+1)^2 interaction thresholds, S+1.
+struct SlowParams {
+    uint32_t xm, xi, sT;
+    int S1;
+};
+__shared__ int2 sOffTbl[32];
+__shared__ SlowParams sSlow;
+
 template <int ARITY>
-__device__ __forceinline__ void build_offset_table(int2* tbl, int P) {
+__device__ __forceinline__ void build_offset_table(int P) {
     for (int e = threadIdx.x; e < Bits<ARITY>::NT; e += blockDim.x) {
         const uint32_t d = static_cast<uint32_t>(e) & (ARITY - 1);
         const int dy = (e >> Bits<ARITY>::DB) & 1, dx = (e >> (Bits<ARITY>::DB + 1)) & 1;
         int dr, dc;
         dir_rc(d, dr, dc);
         const int so = dy * P + dx;
-        tbl[e] = make_int2(so, so + dr * P + dc);
+        sOffTbl[e] = make_int2(so, so + dr * P + dc);
     }
 }
 
-// Per-CTA, per-phase constants of the attempt loop (kept in registers; slow paths get them by value).
+// Offsets of attempt bits `bits` (low LB bits select the table entry).
+template <int ARITY>
+__device__ __forceinline__ uint2 offsets(uint32_t bits) {
+    const int2 o = sOffTbl[bits & (Bits<ARITY>::NT - 1)];
+    return make_uint2(static_cast<uint32_t>(o.x), static_cast<uint32_t>(o.y));
+}
+
+// Per-phase constants of the attempt loop (registers).  c2 is the STEP counter word of the phase;
+// the REFINE word differs only in the domain field.
 struct PhaseCtx {
-    uint32_t tbl;            // smem address of the offset table
-    uint32_t fast;           // attempt bits below this are certain migrations (NARROW fast path)
-    uint32_t xm, xi;         // X_mig, X_int
-    uint32_t sT;             // smem address of the (S+1)^2 interaction thresholds
-    int S1;
-    uint32_t c1, c2ref, c3;  // draw counter words (c2ref: REFINE domain, phase set, attempt 0)
+    uint32_t fast;       // attempt bits below this are certain migrations (NARROW fast path)
+    uint32_t xm, xi;     // X_mig, X_int (WIDE rule)
+    uint32_t c1, c2, c3;  // draw counter words
 };
+constexpr uint32_t kStepToRefine = (0u ^ 1u) << 16;  // kDomStep ^ kDomRefine in the domain field
 
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
     uint32_t v;
@@ -190,8 +206,8 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 }
 
 // REFINE-domain word of attempt a of `tile` (exact action completion; rare).
-__device__ __noinline__ uint32_t refine_word(uint32_t tile, int a, uint32_t c1, uint32_t c2ref, uint32_t c3) {
-    return philox(tile, c1, c2ref | (static_cast<uint32_t>(a) << 24), c3).x;
+__device__ __noinline__ uint32_t refine_word(uint32_t tile, int a, uint32_t c1, uint32_t c2, uint32_t c3) {
+    return philox(tile, c1, (c2 ^ kStepToRefine) | (static_cast<uint32_t>(a) << 24), c3).x;
 }
 
 // The rule (engine.hpp:111-140) on (s, n) with the exact 32-bit action word x:
@@ -241,22 +257,20 @@ __device__ __forceinline__ uint32_t rule_exact_s(uint32_t s, uint32_t n, uint32_
 // WIDE exact path: the low LB bits come from REFINE (taken only when a consulted threshold
 // shares the coarse value of the word).
 template <int ARITY>
-__device__ __noinline__ uint32_t slow_wide(uint32_t s, uint32_t n, uint32_t word, uint32_t tile, int a, uint32_t xm,
-                                           uint32_t xi, uint32_t sT, int S1, uint32_t c1, uint32_t c2ref,
-                                           uint32_t c3) {
+__device__ __noinline__ uint32_t slow_wide(uint32_t s, uint32_t n, uint32_t word, uint32_t tile, int a, uint32_t c1,
+                                           uint32_t c2, uint32_t c3) {
     constexpr int LB = Bits<ARITY>::LB;
-    const uint32_t x = ((word >> LB) << LB) | (refine_word(tile, a, c1, c2ref, c3) & ((1u << LB) - 1u));
-    return rule_exact_s(s, n, x, xm, xi, sT, S1);
+    const uint32_t x = ((word >> LB) << LB) | (refine_word(tile, a, c1, c2, c3) & ((1u << LB) - 1u));
+    return rule_exact_s(s, n, x, sSlow.xm, sSlow.xi, sSlow.sT, sSlow.S1);
 }
 
 // NARROW slow path: x = coarse(16-LB bits) << (16+LB) | low (16+LB) bits of the REFINE word.
 template <int ARITY>
 __device__ __noinline__ uint32_t slow_narrow(uint32_t s, uint32_t n, uint32_t half, uint32_t tile, int a,
-                                             uint32_t xm, uint32_t xi, uint32_t sT, int S1, uint32_t c1,
-                                             uint32_t c2ref, uint32_t c3) {
+                                             uint32_t c1, uint32_t c2, uint32_t c3) {
     constexpr int LB = Bits<ARITY>::LB, SH = 16 + LB;
-    const uint32_t x = ((half >> LB) << SH) | (refine_word(tile, a, c1, c2ref, c3) & ((1u << SH) - 1u));
-    return rule_exact_s(s, n, x, xm, xi, sT, S1);
+    const uint32_t x = ((half >> LB) << SH) | (refine_word(tile, a, c1, c2, c3) & ((1u << SH) - 1u));
+    return rule_exact_s(s, n, x, sSlow.xm, sSlow.xi, sSlow.sT, sSlow.S1);
 }
 
 // WIDE rule on the coarse word (low LB bits zero).  A comparison against threshold T is decided by
@@ -278,7 +292,8 @@ __device__ __forceinline__ uint32_t rule_wide(uint32_t s, uint32_t n, uint32_t w
             else if (s == 0u)
                 ns = n;
         } else if ((s != 0u) & (n != 0u) & (s != n)) {
-            const uint32_t t1 = lds32(C.sT + 4u * (s * C.S1 + n)), t2 = lds32(C.sT + 4u * (n * C.S1 + s));
+            const uint32_t sT = sSlow.sT, S1 = static_cast<uint32_t>(sSlow.S1);
+            const uint32_t t1 = lds32(sT + 4u * (s * S1 + n)), t2 = lds32(sT + 4u * (n * S1 + s));
             exact = (x == (t1 & HI)) | (x == (t2 & HI));
             if (x < t1)
                 nn = 0u;
@@ -286,14 +301,14 @@ __device__ __forceinline__ uint32_t rule_wide(uint32_t s, uint32_t n, uint32_t w
                 ns = 0u;
         }
     }
-    if (exact) return slow_wide<ARITY>(s, n, word, tile, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+    if (exact) return slow_wide<ARITY>(s, n, word, tile, a, C.c1, C.c2, C.c3);
     return ns | (nn << 8);
 }
 
 // One attempt: `bits` is the 32-bit word (WIDE) or the zero-extended 16-bit half (NARROW).
 template <int ARITY, bool NARROW>
 __device__ __forceinline__ void attempt(uint32_t bits, uint32_t base, uint32_t tile, int a, const PhaseCtx& C) {
-    const uint2 t = lds64(C.tbl + ((bits & (Bits<ARITY>::NT - 1)) << 3));
+    const uint2 t = offsets<ARITY>(bits);
     const uint32_t sa = base + t.x, na = base + t.y;
     const uint32_t s = lds8(sa), n = lds8(na);
     if (NARROW) {
@@ -304,7 +319,7 @@ __device__ __forceinline__ void attempt(uint32_t bits, uint32_t base, uint32_t t
             }
             return;
         }
-        const uint32_t r = slow_narrow<ARITY>(s, n, bits, tile, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+        const uint32_t r = slow_narrow<ARITY>(s, n, bits, tile, a, C.c1, C.c2, C.c3);
         sts8(sa, r & 0xFFu);
         sts8(na, r >> 8);
     } else {
@@ -361,15 +376,14 @@ __device__ __forceinline__ void tile_dual_ordered(const uint32_t (&bA)[4], uint3
     if ((bA[0] ^ bA[1] ^ bA[2] ^ bA[3] ^ bB[0] ^ bB[1] ^ bB[2] ^ bB[3]) == 0x12345u) sts8(baseA, tA);
     return;
 #endif
-    constexpr uint32_t M = Bits<ARITY>::NT - 1;
-    uint2 oA = lds64(C.tbl + ((bA[0] & M) << 3)), oB = lds64(C.tbl + ((bB[0] & M) << 3));
+    uint2 oA = offsets<ARITY>(bA[0]), oB = offsets<ARITY>(bB[0]);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const uint32_t saA = baseA + oA.x, naA = baseA + oA.y, saB = baseB + oB.x, naB = baseB + oB.y;
         const uint32_t sA = lds8(saA), nA = lds8(naA), sB = lds8(saB), nB = lds8(naB);
         if (a < 3) {  // next attempt's offsets do not depend on the lattice
-            oA = lds64(C.tbl + ((bA[a + 1] & M) << 3));
-            oB = lds64(C.tbl + ((bB[a + 1] & M) << 3));
+            oA = offsets<ARITY>(bA[a + 1]);
+            oB = offsets<ARITY>(bB[a + 1]);
         }
         if (NARROW) {
             const bool fA = bA[a] < C.fast, fB = bB[a] < C.fast;
@@ -379,10 +393,10 @@ __device__ __forceinline__ void tile_dual_ordered(const uint32_t (&bA)[4], uint3
             } else {
                 const uint32_t rA =
                     fA ? (nA | (sA << 8))
-                       : slow_narrow<ARITY>(sA, nA, bA[a], tA, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+                       : slow_narrow<ARITY>(sA, nA, bA[a], tA, a, C.c1, C.c2, C.c3);
                 const uint32_t rB =
                     fB ? (nB | (sB << 8))
-                       : slow_narrow<ARITY>(sB, nB, bB[a], tB, a, C.xm, C.xi, C.sT, C.S1, C.c1, C.c2ref, C.c3);
+                       : slow_narrow<ARITY>(sB, nB, bB[a], tB, a, C.c1, C.c2, C.c3);
                 result_store(saA, naA, sA, nA, rA);
                 result_store(saB, naB, sB, nB, rB);
             }

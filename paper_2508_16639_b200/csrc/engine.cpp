@@ -740,7 +740,15 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         if (choice == ESCG_KERNEL_TILE) {
             h->P = tpitch;
             h->smem = tbytes;
-            h->threads = 512;
+            // ~2.5 items (tile pairs) per thread and phase: small lattices get small CTAs, so more
+            // replicas share an SM and fewer lanes idle (measured: L=64 → 64 threads, L=100 → 128,
+            // L >= 200 → 512)
+            const int64_t items = ((h->H + 3) / 4) * (int64_t)((h->L + 7) / 8);
+            int64_t tt = (items * 2 / 5) / 32 * 32;
+            tt = tt > 448 ? 512 : std::max<int64_t>(64, tt);
+            h->threads = static_cast<int>(tt);
+            if (const char* tv = std::getenv("ESCG_TILE_THREADS"))
+                h->threads = std::max(32, std::min(512, (std::atoi(tv) + 31) / 32 * 32));
         } else {
             h->lat[1].alloc(static_cast<size_t>(h->N) * n_replicas);
             // lattices far beyond one CTA per SM stream through many waves: two 512-thread CTAs per

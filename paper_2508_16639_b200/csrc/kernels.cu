@@ -211,20 +211,28 @@ __device__ void ghost_pass(uint8_t* lat, uint8_t* snap, int H, int L, int P) {
 }
 
 template <int ARITY>
-__device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, uint32_t tbl, uint32_t sT, int S1,
-                                              uint64_t mcs, int p, uint32_t s32) {
+__device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, uint64_t mcs, int p, uint32_t s32) {
     constexpr int LB = Bits<ARITY>::LB;
     PhaseCtx C;
-    C.tbl = tbl;
     C.fast = narrow ? ((rule.xm >> (16 + LB)) << LB) : 0u;
     C.xm = rule.xm;
     C.xi = rule.xi;
-    C.sT = sT;
-    C.S1 = S1;
     C.c1 = static_cast<uint32_t>(mcs);
-    C.c2ref = ctr2(mcs, kDomRefine, static_cast<uint32_t>(p), 0u);
+    C.c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
     C.c3 = s32;
     return C;
+}
+
+// Fill the per-CTA static shared state of the attempt paths (before the first phase barrier).
+template <int ARITY>
+__device__ __forceinline__ void attempt_setup(const RuleArgs& rule, uint32_t sT, int S1, int P) {
+    build_offset_table<ARITY>(P);
+    if (threadIdx.x == 0) {
+        sSlow.xm = rule.xm;
+        sSlow.xi = rule.xi;
+        sSlow.sT = sT;
+        sSlow.S1 = S1;
+    }
 }
 
 // Tile-kernel lattice modes: periodic with H, L ≡ 0 (mod 4); reflecting; periodic with seams.
@@ -241,8 +249,8 @@ __device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint
 #pragma unroll 1
     for (int p = 0; p < np; ++p) {
         const int v = rg.colour(p), cy = v / ax.nc, cx = v - cy * ax.nc;
-        const PhaseCtx C = phase_ctx<ARITY>(rule, 0, tbl, sT, S1, mcs, p, s32);
-        const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+        const PhaseCtx C = phase_ctx<ARITY>(rule, 0, mcs, p, s32);
+        const uint32_t c2 = C.c2;
         const int nty = ay.count(cy), ntx = ax.count(cx), cnt = nty * ntx;
         for (int k = tid; k < cnt; k += nt) {
             const int i = k / ntx, j = k - i * ntx;
@@ -277,8 +285,8 @@ __device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t 
 #pragma unroll 1
     for (int p = 0; p < 4; ++p) {
         const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-        const PhaseCtx C = phase_ctx<ARITY>(rule, narrow, tbl, sT, S1, mcs, p, s32);
-        const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+        const PhaseCtx C = phase_ctx<ARITY>(rule, narrow, mcs, p, s32);
+        const uint32_t c2 = C.c2;
         const int nty = (Ty - cy + 1) >> 1;
         const int ntx = (Tx - cx + 1) >> 1;  // tiles of this colour per tile row
         // items: pairs of same-colour tiles (tx, tx+2) of a row (one NARROW draw, or two WIDE
@@ -377,7 +385,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     const uint32_t s32 = seed32(a.seeds[r]);
 
     for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
-    build_offset_table<ARITY>(tblp, P);
+    attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
     tile_copy<true>(lat, glat, H, L, P);
     __syncthreads();
     if (!REFLECT) {
@@ -451,8 +459,8 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
         for (int p = 0; p < 4; ++p) {
             const int q = 4 * t + p;  // global phase of this launch: validity shrinks 3 cells per phase
             const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-            const PhaseCtx C = phase_ctx<ARITY>(rule, NARROW, tbl, sT, S1, mcs, p, s32);
-            const uint32_t c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+            const PhaseCtx C = phase_ctx<ARITY>(rule, NARROW, mcs, p, s32);
+            const uint32_t c2 = C.c2;
             // footprint rows [2j-oy-1, 2j-oy+2] within [3q, Wh-3q); cols within [ex+3q, Ww-ex-3q)
             const int lo = 3 * q, hiR = Wh - 3 * q, loC = ex + 3 * q, hiC = Ww - ex - 3 * q;
             const int jmin = (lo + rp.oy + 2) >> 1, jmax = (hiR - 3 + rp.oy) >> 1;
@@ -701,7 +709,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         }
 #endif
         for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
-        build_offset_table<ARITY>(tblp, P);
+        attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
         // the scratch box must hold valid species codes: dummy attempts index the threshold table
         for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
         DIAG_STAMP(1);
@@ -801,7 +809,7 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
 
     const uint32_t s32 = seed32(a.seeds[r]);
     for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
-    build_offset_table<ARITY>(tblp, P);
+    attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
     for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
     const uint32_t mbar = smem_addr(&sMbar);
     if (tid == 0) {
@@ -1036,10 +1044,12 @@ extern "C" __attribute__((visibility("default"))) int escg_diag_timing(unsigned 
 #endif
 }
 
+// Dynamic shared memory available per CTA: the opt-in limit minus a reserve for the kernels'
+// static shared variables (offset table, slow-path parameters, barriers; < 1 KB).
 int max_smem_optin(int device) {
     int v = 0;
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    return v;
+    return v - 1024;
 }
 
 cudaError_t launch_init(const InitArgs& a, cudaStream_t s) {
