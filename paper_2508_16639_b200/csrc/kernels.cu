@@ -517,8 +517,8 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
                     const bool ok1 = ia1 >= imin && ia1 <= imax, ok2 = ia2 >= imin && ia2 <= imax;
                     const uint32_t scr1 = sw ? g.scratch + 8 : g.scratch, scr2 = sw ? g.scratch : g.scratch + 8;
                     int j = j0 + 2 * a0;
-                    int ty = (jb + j) % Ty;
-                    const int dTy = (2 * R) % Ty;
+                    int ty = big ? (jb + j) % Ty : wrap_down(jb + j, Ty, false);
+                    const int dTy = big ? (2 * R) % Ty : 2 * R;  // window rows < Ty: 2R < Ty
                     uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - rp.oy) * P - rp.ox);
                     const uint32_t dRow = static_cast<uint32_t>(4 * R * P);
                     auto draw1 = [&](int ty_) {
