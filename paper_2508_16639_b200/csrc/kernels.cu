@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "crs.cuh"
@@ -662,8 +663,10 @@ __device__ __forceinline__ void store_block(uint8_t* dst, const uint8_t* win, in
 template <int ARITY>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
+    // Programmatic dependent launch: let the next launch's CTAs start their prologue as soon as SMs
+    // free up; everything that reads the previous launch's output sits behind griddepcontrol.wait.
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int r = blockIdx.z;
-    if (a.run.status[r] != kStatusRunning) return;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
     const int My = margin_rows(a.nmcs), Mx = margin_cols(a.nmcs);
@@ -693,13 +696,20 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         const int wy0 = a.wrap_rows ? ((ry0 - My) % H + H) % H : ry0 - My;  // bands: halo rows, no wrap
         const int wx0 = ((rx0 - Mx) % L + L) % L;
         const uint32_t mbar = smem_addr(&sMbar);
+        // prologue: inputs that no earlier launch writes (rule, seeds, geometry)
+        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+        attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
+        // the scratch box must hold valid species codes: dummy attempts index the threshold table
+        for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
+        if (tma && tid == 0) {
+            mbar_init(mbar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) {
-            if (tid == 0) {
-                mbar_init(mbar, 1);
-                asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-                mbar_expect_tx_arrive(mbar, static_cast<uint32_t>(Wh * Ww));
-            }
+            if (tid == 0) mbar_expect_tx_arrive(mbar, static_cast<uint32_t>(Wh * Ww));
             __syncthreads();
             load_window_tma(win, src, H, L, P, Wh, Ww, wy0, wx0, mbar);
         } else if (v16) {
@@ -708,10 +718,6 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
             load_window<4>(win, src, H, L, P, Wh, Ww, wy0, wx0);
         }
 #endif
-        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
-        attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
-        // the scratch box must hold valid species codes: dummy attempts index the threshold table
-        for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
         DIAG_STAMP(1);
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) mbar_wait(mbar, 0);
@@ -746,6 +752,9 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
             store_block<4>(dst, win, L, P, bh, bw, ry0, rx0, My, Mx);
         }
 #endif
+    } else {
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
     }
     if (a.count) {
         for (int v = tid; v <= kMaxSpecies; v += nt) sCnt[v] = 0;
@@ -1095,8 +1104,20 @@ static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cud
         configured_bytes = a.smem_bytes;
     }
     dim3 grid(static_cast<unsigned>(a.nbx), static_cast<unsigned>(a.nby), static_cast<unsigned>(nrep));
-    k<<<grid, threads, a.smem_bytes, s>>>(a);
-    return cudaGetLastError();
+    // programmatic dependent launch (the kernel waits with griddepcontrol.wait before touching the
+    // previous launch's output); ESCG_PDL=0 turns it off
+    static const bool pdl = !(std::getenv("ESCG_PDL") && std::getenv("ESCG_PDL")[0] == '0');
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(static_cast<unsigned>(threads));
+    cfg.dynamicSmemBytes = static_cast<size_t>(a.smem_bytes);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, a);
 }
 
 int block_persistent_capacity(int arity, int threads, int smem_bytes, int device) {
