@@ -77,9 +77,10 @@ def reference_sample(mcs, mode=2, workers=None, seed=1):
 
 
 def cpu_baseline():
-    v, el, w = reference_sample(mcs=20, mode=2)
+    # ~10 s wall on 16 host cores (~2e8 attempts/s): a bounded sample of the L=3200 workload
+    v, el, w = reference_sample(mcs=200, mode=2)
     return {"value": v, "unit": UNIT, "cores": w, "kind": "reference",
-            "sample": "reference run_max_step (ThreadPool(%d)), RPS L=3200 M=1e-4 p0=0.1, 20 MCS window "
+            "sample": "reference run_max_step (ThreadPool(%d)), RPS L=3200 M=1e-4 p0=0.1, 200 MCS window "
                       "from the first density record (%.1f s wall)" % (w, el)}
 
 
