@@ -286,7 +286,10 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     CK(cudaMemcpy(h->d_cols.p, cols.data(), sizeof(int) * cols.size(), cudaMemcpyHostToDevice));
 }
 
-escgd::RuleArgs rule_args(escg_dev* h) { return escgd::RuleArgs{h->th.xm, h->th.xi, h->d_T.p}; }
+escgd::RuleArgs rule_args(escg_dev* h) {
+    const int LB = h->arity == 8 ? 5 : 4;
+    return escgd::RuleArgs{h->th.xm, h->th.xi, h->d_T.p, (h->th.xm >> (16 + LB)) << LB};
+}
 
 escgd::RunArgs run_args(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int tracked, bool trace) {
     escgd::RunArgs r{};

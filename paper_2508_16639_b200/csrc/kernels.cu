@@ -215,7 +215,8 @@ template <int ARITY>
 __device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, uint64_t mcs, int p, uint32_t s32) {
     constexpr int LB = Bits<ARITY>::LB;
     PhaseCtx C;
-    C.fast = narrow ? ((rule.xm >> (16 + LB)) << LB) : 0u;
+    (void)LB;
+    C.fast = narrow ? rule.fast : 0u;
     C.xm = rule.xm;
     C.xi = rule.xi;
     C.c1 = static_cast<uint32_t>(mcs);
@@ -492,7 +493,11 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
                 const int a0 = udiv_small(tid, nu), b = tid - a0 * nu;
                 if (a0 < R && a0 < nj) {
                     // upper half-warp runs its pair's second tile as chain 1 (bank split, tile_dual)
+#ifdef ESCG_DIAG_NO_SWAP
+                    const bool sw = false;
+#else
                     const bool sw = (tid & 16) != 0;
+#endif
                     int ia1, ia2;  // window tile columns of chain 1 / chain 2
                     uint32_t tc1, tc2;  // global tile-column part of the tile ids
                     uint32_t ctrcol = 0;  // NARROW: pair column of the draw counter

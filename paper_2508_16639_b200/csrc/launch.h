@@ -22,6 +22,7 @@ constexpr int kMaxSpecies = 64;
 struct RuleArgs {
     uint32_t xm, xi;       // X_mig, X_int
     const uint32_t* T;     // (S+1)^2 interaction thresholds (device)
+    uint32_t fast;         // NARROW certain-migration bound on attempt bits: (xm >> (16+LB)) << LB
 };
 
 // Per-replica run bookkeeping (device arrays, length n_replicas unless noted).

@@ -12,6 +12,7 @@ VARIANTS = {
     "enum_only": ["ESCG_DIAG_NO_ATTEMPTS", "ESCG_DIAG_CHEAP_RNG"],
     "no_load": ["ESCG_DIAG_NO_LOAD"],
     "no_phase_sync": ["ESCG_DIAG_NO_PHASE_SYNC"],
+    "no_swap": ["ESCG_DIAG_NO_SWAP"],
 }
 
 if __name__ == "__main__":
