@@ -246,14 +246,18 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     sms *= cta_per_sm;
     smem_cap = std::min(smem_cap, (228 * 1024) / cta_per_sm - 1024);
     const int cu = (h->L % 16 == 0) ? 16 : ((h->L % 8 == 0) ? 8 : 4);
-    const int uy = h->rows_count / 4, ux = h->L / cu;
+    // units: rows in 4s, columns in cu; a remainder (reflecting lattices of any size) joins the last
+    // block, so split boundaries stay even (window origins even: tile parity = global parity)
+    const int uy = std::max(1, h->rows_count / 4), ux = std::max(1, h->L / cu);
+    const int ry_extra = h->rows_count - uy * 4, rx_extra = h->L - ux * cu;
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
     const double kOverheadCells = 40000.0;  // launch + window load/store, measured on B200
     for (int k = 1; k <= kmax; ++k) {
         for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
             for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
-                const int bh = ((uy + nby - 1) / nby) * 4, bw = ((ux + nbx - 1) / nbx) * cu;
+                const int bh = ((uy + nby - 1) / nby) * 4 + std::max(0, ry_extra),
+                          bw = ((ux + nbx - 1) / nbx) * cu + std::max(0, rx_extra);
                 if (block_smem(bh, bw, h->S1, k, nullptr) > static_cast<size_t>(smem_cap)) continue;
                 const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
                 const int64_t waves = (ctas + sms - 1) / sms;
@@ -274,6 +278,8 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     std::vector<int> rows(bnby + 1), cols(bnbx + 1);
     for (int i = 0; i <= bnby; ++i) rows[i] = h->rows_begin + static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
     for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(ux) * i / bnbx) * cu;
+    rows[bnby] = h->rows_begin + h->rows_count;
+    cols[bnbx] = h->L;
     int bh = 0, bw = 0;
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
@@ -365,6 +371,7 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.Hg = h->Hg;
     a.row0 = h->row0;
     a.wrap_rows = h->wrap_rows;
+    a.reflect = h->flux ? 0 : 1;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -406,6 +413,7 @@ escgd::PersistArgs persist_args(escg_dev* h, const escgd::RunArgs& run) {
     a.Hg = h->Hg;
     a.row0 = h->row0;
     a.wrap_rows = h->wrap_rows;
+    a.reflect = h->flux ? 0 : 1;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -492,6 +500,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.Hg = h->Hg;
         a.row0 = h->row0;
         a.wrap_rows = h->wrap_rows;
+        a.reflect = h->flux ? 0 : 1;
         a.nby = h->nby;
         a.nbx = h->nbx;
         a.row_split = h->d_rows.p;
@@ -717,9 +726,7 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         if (choice == ESCG_KERNEL_AUTO) choice = tbytes <= smem_cap ? ESCG_KERNEL_TILE : ESCG_KERNEL_BLOCK;
         if (choice == ESCG_KERNEL_TILE && tbytes > smem_cap)
             config_error("lattice too large for the shared-memory tile kernel");
-        if (choice == ESCG_KERNEL_BLOCK && !h->flux)
-            config_error("block kernel supports periodic (flux) lattices only");
-        if (choice == ESCG_KERNEL_BLOCK && !periodic4)
+        if (choice == ESCG_KERNEL_BLOCK && h->flux && !periodic4)
             config_error("block kernel needs L and H divisible by 4 (lattices with seams run on the tile kernel, "
                          "which holds them up to its shared-memory size)");
         h->kernel = choice;
@@ -771,7 +778,7 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             const bool geom_ok = h->L % 16 == 0 && h->bw_max % 16 == 0 &&
                                  h->bh_max + 2 * escgd::margin_rows(h->kmcs) <= h->H &&
                                  h->bw_max + 2 * escgd::margin_cols(h->kmcs) <= h->L;
-            if (!env_off && geom_ok && h->wrap_rows) {
+            if (!env_off && geom_ok && h->wrap_rows && h->flux) {
                 const int cap = escgd::block_persistent_capacity(h->arity, h->threads, h->smem, device);
                 h->persist = h->nby * h->nbx * n_replicas <= cap;
             }
@@ -1143,6 +1150,7 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 a.Hg = h->Hg;
                 a.row0 = h->row0;
                 a.wrap_rows = h->wrap_rows;
+                a.reflect = h->flux ? 0 : 1;
                 a.nby = h->nby;
                 a.nbx = h->nbx;
                 a.row_split = h->d_rows.p;

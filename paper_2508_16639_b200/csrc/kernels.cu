@@ -665,7 +665,91 @@ __device__ __forceinline__ void store_block(uint8_t* dst, const uint8_t* win, in
     }
 }
 
+// ---- reflecting lattices (flux = false) on the block kernel --------------------------------------
+// Windows are clipped at the lattice edge (no wrap); a clipped side needs no validity margin.  Tiles
+// follow the reflect tiling of orc_crs_run (T = (n + o + 1) / 2 per axis, partial edge tiles), WIDE
+// draws.  Pairs whose footprints stay inside the lattice take the fast dual path; pairs touching the
+// mirror go through tile_reflect (explicit coordinates, reflected neighbours, skipped cells).
 template <int ARITY>
+__device__ void block_phases_reflect(const RuleArgs& rule, uint32_t win0, int H, int L, int P, int nmcs,
+                                     int64_t mcs0, int Wh, int Ww, int wy0, int wx0, int ex, uint32_t s32) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const bool top = wy0 == 0, bot = wy0 + Wh == H, lft = wx0 == 0, rgt = wx0 + Ww == L;
+    const int jb = wy0 >> 1, ib = wx0 >> 1;  // window origin is even: tile parity = global parity
+#pragma unroll 1
+    for (int t = 0; t < nmcs; ++t) {
+        const uint64_t mcs = static_cast<uint64_t>(mcs0 + t);
+        const Round rp = round_params(s32, mcs);
+        const int Ty = (H + rp.oy + 1) >> 1, Tx = (L + rp.ox + 1) >> 1;
+#pragma unroll 1
+        for (int p = 0; p < 4; ++p) {
+            const int q = 4 * t + p;
+            const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
+            const PhaseCtx C = phase_ctx<ARITY>(rule, 0, mcs, p, s32);
+            const int jlo = top ? 0 : ((3 * q + rp.oy + 2) >> 1);
+            const int jhi = bot ? (Ty - 1 - jb) : ((Wh - 3 * q - 3 + rp.oy) >> 1);
+            const int ilo = lft ? 0 : ((ex + 3 * q + rp.ox + 2) >> 1);
+            const int ihi = rgt ? (Tx - 1 - ib) : ((Ww - ex - 3 * q - 3 + rp.ox) >> 1);
+            const int j0 = jlo + ((jlo ^ cy) & 1), i0 = ilo + ((ilo ^ cx) & 1);
+            const int nj = jhi >= j0 ? ((jhi - j0) >> 1) + 1 : 0;
+            const int ni = ihi >= i0 ? ((ihi - i0) >> 1) + 1 : 0;
+            const int nu = (ni + 1) >> 1;  // pairs (i, i + 2) of a row
+            const int cnt = nj * nu;
+            for (int k = tid; k < cnt; k += nt) {
+                const int a_ = udiv_small(k, nu), b_ = k - a_ * nu;
+                const int j = j0 + 2 * a_, iA = i0 + 4 * b_, iB = iA + 2;
+                const bool hasB = iB <= ihi;
+                const int tg = j + jb, sA = iA + ib, sB = iB + ib;
+                const int y0 = 2 * tg - rp.oy, xA = 2 * sA - rp.ox, xB = 2 * sB - rp.ox;
+                const uint32_t tA = static_cast<uint32_t>(tg) * static_cast<uint32_t>(Tx) + static_cast<uint32_t>(sA);
+                const uint32_t tB = tA + 2;
+                const uint4 wA = philox(tA, C.c1, C.c2, s32);
+                const uint4 wB = hasB ? philox(tB, C.c1, C.c2, s32) : make_uint4(0, 0, 0, 0);
+                const bool inR = y0 >= 1 && y0 + 2 <= H - 1;
+                const bool inA = inR && xA >= 1 && xA + 2 <= L - 1, inB = inR && xB >= 1 && xB + 2 <= L - 1;
+                const uint32_t rowb = win0 + static_cast<uint32_t>((y0 - wy0) * P - wx0);
+                if (inA && hasB && inB) {
+                    const uint32_t b1[4] = {wA.x, wA.y, wA.z, wA.w};
+                    const uint32_t b2[4] = {wB.x, wB.y, wB.z, wB.w};
+                    tile_dual_ordered<ARITY, false>(b1, rowb + xA, tA, b2, rowb + xB, tB, C);
+                } else {
+                    tile_reflect<ARITY>(wA, win0, y0, xA, -wy0, -wx0, P, H, L, tA, C);
+                    if (hasB) tile_reflect<ARITY>(wB, win0, y0, xB, -wy0, -wx0, P, H, L, tB, C);
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Plain (non-wrapping) copies of a rows x cols region between global memory (pitch L) and the window
+// (pitch P): 4-byte words when everything is 4-aligned, else bytes.
+template <bool TO_WIN>
+__device__ void copy_region(uint8_t* win, int P, uint8_t* glob, int L, int rows, int cols) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool w4 = ((L | P | cols) & 3) == 0 && ((reinterpret_cast<uintptr_t>(glob) | reinterpret_cast<uintptr_t>(win)) & 3) == 0;
+    for (int y = warp; y < rows; y += nw) {
+        uint8_t* g = glob + static_cast<size_t>(y) * L;
+        uint8_t* w = win + y * P;
+        if (w4) {
+            for (int c = lane; c < (cols >> 2); c += 32) {
+                if (TO_WIN)
+                    reinterpret_cast<uint32_t*>(w)[c] = __ldcg(reinterpret_cast<const unsigned int*>(g) + c);
+                else
+                    __stcg(reinterpret_cast<unsigned int*>(g) + c, reinterpret_cast<const uint32_t*>(w)[c]);
+            }
+        } else {
+            for (int c = lane; c < cols; c += 32) {
+                if (TO_WIN)
+                    w[c] = g[c];
+                else
+                    g[c] = w[c];
+            }
+        }
+    }
+}
+
+template <int ARITY, bool REFLECT>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     // Programmatic dependent launch: let the next launch's CTAs start their prologue as soon as SMs
@@ -696,7 +780,19 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     const bool tma = v16 && Wh <= H && Ww <= L;
     DIAG_STAMP(0);
 
-    if (a.step) {
+    if (REFLECT && a.step) {
+        const uint32_t s32 = seed32(a.seeds[r]);
+        const int wy0 = max(0, ry0 - My), wx0 = max(0, rx0 - Mx);
+        const int wh = min(H, ry1 + My) - wy0, ww = min(L, rx1 + Mx) - wx0;
+        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+        attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
+        copy_region<true>(win, P, const_cast<uint8_t*>(src) + static_cast<size_t>(wy0) * L + wx0, L, wh, ww);
+        __syncthreads();
+        block_phases_reflect<ARITY>(a.rule, smem_addr(win), H, L, P, a.nmcs, a.mcs, wh, ww, wy0, wx0, Mx - My, s32);
+        copy_region<false>(win + (ry0 - wy0) * P + (rx0 - wx0), P, dst + static_cast<size_t>(ry0) * L + rx0, L, bh, bw);
+    } else if (a.step) {
         const uint32_t s32 = seed32(a.seeds[r]);
         const int wy0 = a.wrap_rows ? ((ry0 - My) % H + H) % H : ry0 - My;  // bands: halo rows, no wrap
         const int wx0 = ((rx0 - Mx) % L + L) % L;
@@ -764,7 +860,9 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     if (a.count) {
         for (int v = tid; v <= kMaxSpecies; v += nt) sCnt[v] = 0;
         __syncthreads();
-        if (a.step)
+        if (a.step && REFLECT)
+            block_count(win + (ry0 - max(0, ry0 - My)) * P + (rx0 - max(0, rx0 - Mx)), bh, bw, P, S1, sCnt);
+        else if (a.step)
             block_count(win + My * P + Mx, bh, bw, P, S1, sCnt);
         else
             block_count(src + static_cast<size_t>(ry0) * L + rx0, bh, bw, L, S1, sCnt);
@@ -1099,10 +1197,10 @@ cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s
     return tile_launch_t<4, kModePeriodic>(a, nrep, threads, s);
 }
 
-template <int ARITY>
+template <int ARITY, bool REFLECT>
 static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {
     static int configured_bytes = -1;
-    auto k = block_kernel<ARITY>;
+    auto k = block_kernel<ARITY, REFLECT>;
     if (configured_bytes < a.smem_bytes) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
         if (e != cudaSuccess) return e;
@@ -1149,7 +1247,9 @@ cudaError_t launch_block_persistent(const PersistArgs& a, int nrep, int threads,
 }
 
 cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {
-    return a.arity == 8 ? block_launch_t<8>(a, nrep, threads, s) : block_launch_t<4>(a, nrep, threads, s);
+    if (a.reflect)
+        return a.arity == 8 ? block_launch_t<8, true>(a, nrep, threads, s) : block_launch_t<4, true>(a, nrep, threads, s);
+    return a.arity == 8 ? block_launch_t<8, false>(a, nrep, threads, s) : block_launch_t<4, false>(a, nrep, threads, s);
 }
 
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s) {

@@ -387,3 +387,35 @@ def test_seam_lattices_reject_block_kernel(escg):
     p = params(escg, 3, 8, 3, 1e-4, 0.1, 4, True)
     with pytest.raises(escg.ConfigError, match=">= 4"):
         escg.DeviceEngine(p, escg.make_circulant(3, [1]))
+
+
+@pytest.mark.parametrize("LH,arity,kmcs,name", [((64, 64), 4, 2, "rps"), ((101, 67), 8, 1, "rps"), ((13, 6), 4, 1, "rps"),
+                                                 ((600, 500), 4, 2, "rps"), ((603, 498), 8, 3, "park8"),
+                                                 ((1000, 31), 4, 4, "rpsls"), ((2, 2), 4, 1, "rps")])
+def test_block_kernel_reflect_matches_crs_oracle(escg, oracle, LH, arity, kmcs, name, monkeypatch):
+    """Mirror-reflecting lattices (flux=false) on the block kernel: clipped windows, reflect tiling,
+    boundary pairs through the explicit-coordinate path — bit-exact with the sequential oracle."""
+    L, H = LH
+    monkeypatch.setenv("ESCG_BLOCK_MCS", str(kmcs))
+    model = model_of(escg, name)
+    S = model.size
+    M = 0.0 if name == "park8" else 1e-3
+    p = params(escg, L, H, S, M, 0.1, arity, False, seed=4242)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        assert eng.describe()["kernel"] == "block" and eng.draw_format() == "wide"
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(7)
+        got = eng.get_lattice()
+        st = eng.run(12, interval=3, record_trace=True)
+        steps, counts = eng.read_trace(0)
+        final = eng.get_lattice()
+    want = oracle.crs_run(init, L, H, model.matrix(), M, 4242, 0, 7, arity=arity, flux=False)
+    assert np.array_equal(got, want)
+    if st[0] == escg.RunStatus.Stasis:  # tiny lattices collapse at the first record
+        assert np.array_equal(final, want) and steps.tolist() == [7]
+        return
+    want12 = oracle.crs_run(want, L, H, model.matrix(), M, 4242, 7, 5, arity=arity, flux=False)
+    assert np.array_equal(final, want12)
+    assert steps.tolist()[-1] == 12
+    assert counts[-1].tolist() == np.bincount(want12, minlength=S + 1).tolist()
