@@ -1096,8 +1096,25 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 }
             }
         }
-        std::vector<cudaEvent_t> ev_k(n), ev_x(n);
+        // per-band ordering events, destroyed on every exit path
+        struct Events {
+            std::vector<cudaEvent_t> k, x;
+            std::vector<int> dev;
+            ~Events() {
+                for (size_t g = 0; g < k.size(); ++g) {
+                    cudaSetDevice(dev[g]);
+                    if (k[g]) cudaEventDestroy(k[g]);
+                    if (x[g]) cudaEventDestroy(x[g]);
+                }
+            }
+        } ev;
+        ev.k.assign(n, nullptr);
+        ev.x.assign(n, nullptr);
+        ev.dev.assign(n, 0);
+        std::vector<cudaEvent_t>& ev_k = ev.k;
+        std::vector<cudaEvent_t>& ev_x = ev.x;
         for (int g = 0; g < n; ++g) {
+            ev.dev[g] = bands[g]->device;
             CK(cudaSetDevice(bands[g]->device));
             CK(cudaEventCreateWithFlags(&ev_k[g], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_x[g], cudaEventDisableTiming));
@@ -1176,8 +1193,6 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
         for (int g = 0; g < n; ++g) {
             CK(cudaSetDevice(bands[g]->device));
             CK(cudaStreamSynchronize(bands[g]->stream));
-            CK(cudaEventDestroy(ev_k[g]));
-            CK(cudaEventDestroy(ev_x[g]));
             bands[g]->mcs[0] += n_mcs;
             bands[g]->cur[0] = par;
             bands[g]->last_launches = launch_no;

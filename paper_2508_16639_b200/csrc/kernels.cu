@@ -11,6 +11,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -1199,12 +1200,21 @@ cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s
 
 template <int ARITY, bool REFLECT>
 static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {
-    static int configured_bytes = -1;
+    // the dynamic-smem opt-in is a per-device function attribute: remember it per device (band
+    // groups drive several devices from one thread); atomics keep concurrent host threads safe
+    static std::atomic<int> configured_bytes[kMaxDevices];
     auto k = block_kernel<ARITY, REFLECT>;
-    if (configured_bytes < a.smem_bytes) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= kMaxDevices || configured_bytes[dev].load() < a.smem_bytes) {
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
         if (e != cudaSuccess) return e;
-        configured_bytes = a.smem_bytes;
+        if (dev >= 0 && dev < kMaxDevices) {
+            int cur = configured_bytes[dev].load();
+            while (cur < a.smem_bytes && !configured_bytes[dev].compare_exchange_weak(cur, a.smem_bytes)) {
+            }
+        }
     }
     dim3 grid(static_cast<unsigned>(a.nbx), static_cast<unsigned>(a.nby), static_cast<unsigned>(nrep));
     // programmatic dependent launch (the kernel waits with griddepcontrol.wait before touching the

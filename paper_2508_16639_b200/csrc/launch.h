@@ -18,6 +18,7 @@ __host__ __device__ constexpr int margin_cols(int k) { return (12 * k + 4 + 15) 
 constexpr int kTileR0 = 2;
 constexpr int kTileC0 = 4;
 constexpr int kMaxSpecies = 64;
+constexpr int kMaxDevices = 64;
 
 struct RuleArgs {
     uint32_t xm, xi;       // X_mig, X_int
