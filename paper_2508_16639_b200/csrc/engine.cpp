@@ -186,6 +186,7 @@ struct escg_dev {
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
     int bh_max = 0, bw_max = 0;
+    int seam_np = 0;  // block kernel on a periodic lattice with seams: colour phases per MCS (4, 6, 9)
     // row-band engines (one band of a lattice sharded by rows): the local buffer holds
     // halo + band_rows + halo rows; local row r is global row (row0 + r) mod Hg
     int Hg = 0, row0 = 0, wrap_rows = 1;
@@ -229,7 +230,17 @@ namespace {
 
 // Block-kernel decomposition: row splits at multiples of 4, column splits at multiples of 8 when
 // L % 8 == 0 (keeps NARROW tile pairs aligned), minimising waves x computed window area.
-size_t block_smem(int bh, int bw, int S1, int k, int* pitch) {
+size_t block_smem(int bh, int bw, int S1, int k, int* pitch, int seam_np = 0) {
+    if (seam_np > 0) {
+        // seam mode: margin 3 * phases * k on every side, byte-granular window, per-axis tile lists
+        const int m = 3 * seam_np * k;
+        const int Wh = bh + 2 * m, Ww = bw + 2 * m;
+        const int P = (Ww + 15) & ~15;
+        if (pitch) *pitch = P;
+        return static_cast<size_t>(((Wh * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8 +
+                                   (escgd::kMaxSpecies + 1) * 4 + 4 * P + 64 + 16 +
+                                   3 * 16 * ((Wh / 2 + 2) + (Ww / 2 + 2)));
+    }
     // pitch ≡ 0 (mod 128 bytes): see tile_dual (bank-conflict-light half-warp split)
     const int P = ((bw + 2 * escgd::margin_cols(k)) + 127) & ~127;
     if (pitch) *pitch = P;
@@ -258,10 +269,11 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
             for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
                 const int bh = ((uy + nby - 1) / nby) * 4 + std::max(0, ry_extra),
                           bw = ((ux + nbx - 1) / nbx) * cu + std::max(0, rx_extra);
-                if (block_smem(bh, bw, h->S1, k, nullptr) > static_cast<size_t>(smem_cap)) continue;
+                if (block_smem(bh, bw, h->S1, k, nullptr, h->seam_np) > static_cast<size_t>(smem_cap)) continue;
                 const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
                 const int64_t waves = (ctas + sms - 1) / sms;
-                const double area = (bh + 12.0 * k + 3.0) * (bw + 12.0 * k + 3.0);
+                const double grow = 3.0 * (h->seam_np > 0 ? h->seam_np : 4) * k + 3.0;  // validity margin
+                const double area = (bh + grow) * (bw + grow);
                 const double cost = static_cast<double>(waves) * (area + kOverheadCells / k);
                 if (cost < best * 0.999) {
                     best = cost;
@@ -283,7 +295,7 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     int bh = 0, bw = 0;
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
-    h->smem = static_cast<int>(block_smem(bh, bw, h->S1, bk, &h->P));
+    h->smem = static_cast<int>(block_smem(bh, bw, h->S1, bk, &h->P, h->seam_np));
     h->bh_max = bh;
     h->bw_max = bw;
     h->d_rows.alloc(rows.size());
@@ -372,6 +384,7 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.row0 = h->row0;
     a.wrap_rows = h->wrap_rows;
     a.reflect = h->flux ? 0 : 1;
+    a.seam_np = h->seam_np;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -414,6 +427,7 @@ escgd::PersistArgs persist_args(escg_dev* h, const escgd::RunArgs& run) {
     a.row0 = h->row0;
     a.wrap_rows = h->wrap_rows;
     a.reflect = h->flux ? 0 : 1;
+    a.seam_np = h->seam_np;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -501,6 +515,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.row0 = h->row0;
         a.wrap_rows = h->wrap_rows;
         a.reflect = h->flux ? 0 : 1;
+        a.seam_np = h->seam_np;
         a.nby = h->nby;
         a.nbx = h->nbx;
         a.row_split = h->d_rows.p;
@@ -726,9 +741,10 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         if (choice == ESCG_KERNEL_AUTO) choice = tbytes <= smem_cap ? ESCG_KERNEL_TILE : ESCG_KERNEL_BLOCK;
         if (choice == ESCG_KERNEL_TILE && tbytes > smem_cap)
             config_error("lattice too large for the shared-memory tile kernel");
-        if (choice == ESCG_KERNEL_BLOCK && h->flux && !periodic4)
-            config_error("block kernel needs L and H divisible by 4 (lattices with seams run on the tile kernel, "
-                         "which holds them up to its shared-memory size)");
+        if (choice == ESCG_KERNEL_BLOCK && h->flux && !periodic4) {
+            // seams on the block kernel: 2 or 3 colours per axis
+            h->seam_np = (h->H % 4 == 0 ? 2 : 3) * (h->L % 4 == 0 ? 2 : 3);
+        }
         h->kernel = choice;
         // NARROW (16-bit attempt words, one draw per tile pair) when migrations dominate so much that
         // at most 1/64 of attempts leave the coarse fast path; needs periodic wrap and L % 8 == 0.
@@ -1168,6 +1184,7 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 a.row0 = h->row0;
                 a.wrap_rows = h->wrap_rows;
                 a.reflect = h->flux ? 0 : 1;
+        a.seam_np = h->seam_np;
                 a.nby = h->nby;
                 a.nbx = h->nbx;
                 a.row_split = h->d_rows.p;

@@ -750,8 +750,96 @@ __device__ void copy_region(uint8_t* win, int P, uint8_t* glob, int L, int rows,
     }
 }
 
-template <int ARITY, bool REFLECT>
+// ---- periodic lattices with seams (L or H not divisible by 4) on the block kernel ---------------
+// Per MCS the window's tiles are listed per axis in shared memory (global tile, local start row /
+// column, 1 or 2 cells, colour), built from the seam tiling of SeamAxis/round_params_g for that MCS'
+// origin; each of the 4, 6 or 9 phases then runs the (row list of colour cy) x (column list of
+// colour cx) tiles whose footprints lie in the phase's valid region, as single WIDE tiles.  The
+// validity region shrinks 3 cells per phase, so the margin is 3 * phases * MCS per launch.
+struct SeamEntry {
+    int t, start, nc, pad;
+};
+
+__device__ void seam_axis_lists(SeamEntry* lists, int* counts, int W, int w0, int n, int o, const SeamAxis ax) {
+    // one warp per axis; lists[c * cap + i], cap = W / 2 + 2
+    const int lane = threadIdx.x & 31, cap = W / 2 + 2;
+    int cnt[3] = {0, 0, 0};
+    for (int base = 0; base < W; base += 32) {
+        const int y = base + lane;
+        bool start = false;
+        int t = 0, nc = 0, col = 0;
+        if (y < W) {
+            const int g = (w0 + y) % n;
+            const int pos = (g + o) % n;
+            start = (pos & 1) == 0;
+            t = pos >> 1;
+            nc = pos + 1 < n ? 2 : 1;
+            col = t == ax.seam ? 2 : (t & 1);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const unsigned m = __ballot_sync(0xffffffffu, start && col == c);
+            if (start && col == c) {
+                const int idx = cnt[c] + __popc(m & ((1u << lane) - 1u));
+                if (idx < cap) lists[c * cap + idx] = SeamEntry{t, y, nc, 0};
+            }
+            cnt[c] += __popc(m);
+        }
+    }
+    if (lane == 0)
+        for (int c = 0; c < 3; ++c) counts[c] = min(cnt[c], cap);
+}
+
+template <int ARITY>
+__device__ void block_phases_seam(const RuleArgs& rule, uint32_t win0, int H, int L, int P, int nmcs, int64_t mcs0,
+                                  int Wh, int Ww, int wy0, int wx0, uint32_t s32, SeamEntry* rows, SeamEntry* cols,
+                                  int* counts) {
+    const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5;
+    const SeamAxis ay(H), ax(L);
+    const int np = ay.nc * ax.nc, capy = Wh / 2 + 2, capx = Ww / 2 + 2;
+#pragma unroll 1
+    for (int t = 0; t < nmcs; ++t) {
+        const uint64_t mcs = static_cast<uint64_t>(mcs0 + t);
+        const RoundG rg = round_params_g(s32, mcs, ay.nc, ax.nc);
+        if (warp == 0) seam_axis_lists(rows, counts, Wh, wy0, H, rg.oy, ay);
+        if (warp == 1) seam_axis_lists(cols, counts + 3, Ww, wx0, L, rg.ox, ax);
+        __syncthreads();
+#pragma unroll 1
+        for (int p = 0; p < np; ++p) {
+            const int q = np * t + p;
+            const int v = rg.colour(p), cy = v / ax.nc, cx = v - cy * ax.nc;
+            const PhaseCtx C = phase_ctx<ARITY>(rule, 0, mcs, p, s32);
+            const int ny = counts[cy], nx = counts[3 + cx], cnt = ny * nx;
+            const int lo = 3 * q, hiY = Wh - 3 * q, hiX = Ww - 3 * q;
+            for (int k = tid; k < cnt; k += nt) {
+                const int i = udiv_small(k, nx), j = k - i * nx;
+                const SeamEntry R = rows[cy * capy + i], Cc = cols[cx * capx + j];
+                // footprint [start - 1, start + nc] inside the valid region of this phase
+                if (R.start - 1 < lo || R.start + R.nc > hiY - 1 || Cc.start - 1 < lo || Cc.start + Cc.nc > hiX - 1)
+                    continue;
+                const uint32_t tile = static_cast<uint32_t>(R.t) * static_cast<uint32_t>(ax.T) + static_cast<uint32_t>(Cc.t);
+                const uint32_t base = win0 + static_cast<uint32_t>(R.start * P + Cc.start);
+                tile_seam<ARITY>(philox(tile, C.c1, C.c2, s32), base, tile, R.nc == 1, Cc.nc == 1, C);
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Wrapping byte copy of a window (any L; windows may wrap several times around small axes).
+__device__ void load_window_bytes(uint8_t* win, const uint8_t* src, int H, int L, int P, int Wh, int Ww, int wy0,
+                                  int wx0) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int y = warp; y < Wh; y += nw) {
+        const uint8_t* srow = src + static_cast<size_t>((wy0 + y) % H) * L;
+        uint8_t* drow = win + y * P;
+        for (int x = lane; x < Ww; x += 32) drow[x] = srow[(wx0 + x) % L];
+    }
+}
+
+template <int ARITY, int BMODE>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
+    constexpr bool REFLECT = BMODE == 1, SEAM = BMODE == 2;
     extern __shared__ __align__(128) uint8_t smem[];
     // Programmatic dependent launch: let the next launch's CTAs start their prologue as soon as SMs
     // free up; everything that reads the previous launch's output sits behind griddepcontrol.wait.
@@ -759,7 +847,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     const int r = blockIdx.z;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
-    const int My = margin_rows(a.nmcs), Mx = margin_cols(a.nmcs);
+    const int My = SEAM ? 3 * a.seam_np * a.nmcs : margin_rows(a.nmcs), Mx = SEAM ? My : margin_cols(a.nmcs);
     const int ry0 = a.row_split[blockIdx.y], ry1 = a.row_split[blockIdx.y + 1];
     const int rx0 = a.col_split[blockIdx.x], rx1 = a.col_split[blockIdx.x + 1];
     const int bh = ry1 - ry0, bw = rx1 - rx0;
@@ -781,7 +869,23 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     const bool tma = v16 && Wh <= H && Ww <= L;
     DIAG_STAMP(0);
 
-    if (REFLECT && a.step) {
+    if (SEAM && a.step) {
+        const uint32_t s32 = seed32(a.seeds[r]);
+        const int wy0 = ((ry0 - My) % H + H) % H, wx0 = ((rx0 - Mx) % L + L) % L;
+        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+        attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
+        SeamEntry* rows = reinterpret_cast<SeamEntry*>(
+            (reinterpret_cast<uintptr_t>(sScratch) + 4 * P + 15) & ~static_cast<uintptr_t>(15));
+        SeamEntry* cols = rows + 3 * (Wh / 2 + 2);
+        __shared__ int sSeamCnt[6];
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
+        load_window_bytes(win, src, H, L, P, Wh, Ww, wy0, wx0);
+        __syncthreads();
+        block_phases_seam<ARITY>(a.rule, smem_addr(win), H, L, P, a.nmcs, a.mcs, Wh, Ww, wy0, wx0, s32, rows, cols,
+                                 sSeamCnt);
+        copy_region<false>(win + My * P + Mx, P, dst + static_cast<size_t>(ry0) * L + rx0, L, bh, bw);
+    } else if (REFLECT && a.step) {
         const uint32_t s32 = seed32(a.seeds[r]);
         const int wy0 = max(0, ry0 - My), wx0 = max(0, rx0 - Mx);
         const int wh = min(H, ry1 + My) - wy0, ww = min(L, rx1 + Mx) - wx0;
@@ -1198,12 +1302,12 @@ cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s
     return tile_launch_t<4, kModePeriodic>(a, nrep, threads, s);
 }
 
-template <int ARITY, bool REFLECT>
+template <int ARITY, int BMODE>
 static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {
     // the dynamic-smem opt-in is a per-device function attribute: remember it per device (band
     // groups drive several devices from one thread); atomics keep concurrent host threads safe
     static std::atomic<int> configured_bytes[kMaxDevices];
-    auto k = block_kernel<ARITY, REFLECT>;
+    auto k = block_kernel<ARITY, BMODE>;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
@@ -1258,8 +1362,10 @@ cudaError_t launch_block_persistent(const PersistArgs& a, int nrep, int threads,
 
 cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {
     if (a.reflect)
-        return a.arity == 8 ? block_launch_t<8, true>(a, nrep, threads, s) : block_launch_t<4, true>(a, nrep, threads, s);
-    return a.arity == 8 ? block_launch_t<8, false>(a, nrep, threads, s) : block_launch_t<4, false>(a, nrep, threads, s);
+        return a.arity == 8 ? block_launch_t<8, 1>(a, nrep, threads, s) : block_launch_t<4, 1>(a, nrep, threads, s);
+    if (a.seam_np > 0)
+        return a.arity == 8 ? block_launch_t<8, 2>(a, nrep, threads, s) : block_launch_t<4, 2>(a, nrep, threads, s);
+    return a.arity == 8 ? block_launch_t<8, 0>(a, nrep, threads, s) : block_launch_t<4, 0>(a, nrep, threads, s);
 }
 
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s) {

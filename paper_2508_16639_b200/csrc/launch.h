@@ -67,6 +67,7 @@ struct BlockArgs {
     int row0;            // global row of local row 0 (band engines: band start - halo, mod Hg)
     int wrap_rows;       // 1: the local buffer is the whole periodic lattice; 0: band with halo rows
     int reflect;         // 1: mirror-reflecting lattice (flux = false): clipped windows, reflect tiling
+    int seam_np;         // > 0: periodic lattice with seams (L or H not divisible by 4): phases per MCS
     int nby, nbx;
     const int* row_split;  // nby+1 row boundaries (multiples of 4)
     const int* col_split;  // nbx+1

@@ -380,10 +380,7 @@ def test_seam_lattice_ensemble_matches_oracle(escg, oracle):
 
 
 @pytest.mark.gpu
-def test_seam_lattices_reject_block_kernel(escg):
-    p = params(escg, 1002, 1000, 3, 1e-4, 0.1, 4, True)
-    with pytest.raises(escg.ConfigError, match="divisible by 4"):
-        escg.DeviceEngine(p, escg.make_circulant(3, [1]), kernel="block")
+def test_periodic_lattices_need_four_cells_per_side(escg):
     p = params(escg, 3, 8, 3, 1e-4, 0.1, 4, True)
     with pytest.raises(escg.ConfigError, match=">= 4"):
         escg.DeviceEngine(p, escg.make_circulant(3, [1]))
@@ -419,3 +416,34 @@ def test_block_kernel_reflect_matches_crs_oracle(escg, oracle, LH, arity, kmcs, 
     assert np.array_equal(final, want12)
     assert steps.tolist()[-1] == 12
     assert counts[-1].tolist() == np.bincount(want12, minlength=S + 1).tolist()
+
+
+@pytest.mark.parametrize("LH,arity,kmcs,name", [((1002, 1000), 4, 1, "rps"), ((501, 463), 8, 1, "park8"),
+                                                 ((50, 50), 4, 2, "rps"), ((21, 15), 8, 1, "rps"),
+                                                 ((7, 6), 4, 1, "rpsls"), ((1000, 30), 4, 2, "rps"),
+                                                 ((30, 1001), 8, 1, "rps")])
+def test_block_kernel_seams_match_crs_oracle(escg, oracle, LH, arity, kmcs, name, monkeypatch):
+    """Periodic lattices with seams on the block kernel (per-axis tile lists, 6/9 phases, margin
+    3 x phases x MCS; small lattices make windows wrap several times) — bit-exact with the oracle."""
+    L, H = LH
+    monkeypatch.setenv("ESCG_BLOCK_MCS", str(kmcs))
+    model = model_of(escg, name)
+    S = model.size
+    M = 0.0 if name == "park8" else 1e-3
+    p = params(escg, L, H, S, M, 0.1, arity, True, seed=777)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        assert eng.describe()["kernel"] == "block" and eng.draw_format() == "wide"
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(5)
+        got = eng.get_lattice()
+        st = eng.run(9, interval=2, record_trace=True)
+        steps, counts = eng.read_trace(0)
+        final = eng.get_lattice()
+    want = oracle.crs_run(init, L, H, model.matrix(), M, 777, 0, 5, arity=arity)
+    assert np.array_equal(got, want)
+    if st[0] == escg.RunStatus.Stasis:
+        return
+    want9 = oracle.crs_run(want, L, H, model.matrix(), M, 777, 5, 4, arity=arity)
+    assert np.array_equal(final, want9)
+    assert steps.tolist()[-1] == 9 and counts[-1].tolist() == np.bincount(want9, minlength=S + 1).tolist()
