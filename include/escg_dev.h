@@ -163,6 +163,15 @@ ESCG_API int escg_dev_band_info(escg_dev* h, int32_t* band_start, int32_t* band_
 /* Advance a whole band group (bands[g] = band g; any mix of devices) by n_mcs: per chunk, halo
  * exchange by peer copies between ring neighbours, then the block kernel on every band. */
 ESCG_API int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs);
+/* Primitives of a multi-process band group (one rank per GPU, halos moved by the caller, e.g. NCCL
+ * send/recv): device pointers into the band's current buffer — the top halo rows, the first
+ * `halo` band rows (sent up), the last `halo` band rows (sent down), the bottom halo rows — and the
+ * byte count of each (halo * L).  Valid until the next escg_dev_band_step. */
+ESCG_API int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint8_t** send_bot,
+                                uint8_t** recv_bot, int64_t* bytes);
+/* One chunk (1 <= n_mcs <= kmcs) of MCS on this band alone; the halos must hold the neighbours'
+ * current rows.  Synchronous. */
+ESCG_API int escg_dev_band_step(escg_dev* h, int32_t n_mcs);
 
 /* One-call mirror of escg::simulate(params, model, mode, …) (engine.cpp:194-240) for a single
  * lattice: initialise on device (or resume from resume_cells at resume_mcs), run to completion

@@ -104,3 +104,103 @@ class BandGroup:
     def advance(self, n_mcs: int):
         arr = (C.c_void_p * self.n)(*[h.value for h in self._h])
         check(lib().escg_group_advance(arr, self.n, int(n_mcs)))
+
+
+# ---- one process per GPU ---------------------------------------------------------------------
+
+def exchange_halos(recv_top, send_top, send_bot, recv_bot, rank: int, world: int, group=None) -> None:
+    """Ring halo exchange of a band group over torch.distributed point-to-point (NCCL on GPUs, gloo
+    on CPU tensors).  Band g's top halo receives the last `halo` rows of band g-1 and its bottom
+    halo the first `halo` rows of band g+1 (periodic ring).  Two shifts, each one send + one recv per
+    rank, so the pairing is unambiguous for any world size >= 2 (world 2: both neighbours are the
+    same rank)."""
+    import torch.distributed as dist
+
+    up, down = (rank - 1) % world, (rank + 1) % world
+    for sends, recvs in (((send_bot, down), (recv_top, up)), ((send_top, up), (recv_bot, down))):
+        ops = [dist.P2POp(dist.isend, sends[0], sends[1], group), dist.P2POp(dist.irecv, recvs[0], recvs[1], group)]
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+
+
+class _DevView:
+    """Zero-copy view of engine-owned device bytes for torch (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3}
+
+
+class DistributedBand:
+    """This rank's band of one lattice sharded by rows over ranks, one process per GPU.
+
+    Each chunk of kmcs MCS: halo rows move between ring neighbours with NCCL send/recv straight
+    from/to the engine's device buffers (exchange_halos), then the block kernel runs on the band
+    (escg_dev_band_step).  Draws depend only on global coordinates, so the sharded run equals the
+    single-lattice run bit for bit."""
+
+    def __init__(self, params: SimParams, model: DominanceModel, rank: int, world: int, device: int = 0, kmcs: int = 2,
+                 group=None):
+        if params.seed is None:
+            raise ConfigError("a band group needs an explicit seed (every band must share it)")
+        if world < 2:
+            raise ConfigError("a distributed band group needs at least 2 ranks")
+        self.params, self.model, self.rank, self.world, self.device, self.group = params, model, rank, world, device, group
+        h = C.c_void_p()
+        check(lib().escg_dev_create_band(C.byref(params.to_c()), np.ascontiguousarray(model.entries, np.float64),
+                                         int(model.size), int(model.kind), int(device), int(world), int(rank),
+                                         int(kmcs), C.byref(h)))
+        self._h = h
+        self.info = BandGroup._band_info(h)
+
+    def close(self):
+        if self._h:
+            lib().escg_dev_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def init_lattice(self):
+        check(lib().escg_dev_init_lattice(self._h))
+
+    def set_band(self, band_cells, mcs: int = 0):
+        """This band's rows (band_rows x L int32) at MCS `mcs`."""
+        part = np.ascontiguousarray(np.asarray(band_cells).ravel(), np.int32)
+        check(lib().escg_dev_set_lattice(self._h, 0, part, int(mcs)))
+
+    def get_band(self) -> np.ndarray:
+        part = np.zeros(self.info["rows"] * self.params.length, np.int32)
+        m = C.c_int64(0)
+        check(lib().escg_dev_get_lattice(self._h, 0, part.ctypes.data_as(C.c_void_p), C.byref(m)))
+        return part
+
+    def counts(self) -> np.ndarray:
+        c = np.zeros(self.model.size + 1, np.uint64)
+        check(lib().escg_dev_counts(self._h, 0, c))
+        return c
+
+    def halo_views(self):
+        """(recv_top, send_top, send_bot, recv_bot) as uint8 CUDA tensors over the current buffer."""
+        import torch
+
+        p = [C.c_void_p() for _ in range(4)]
+        nbytes = C.c_int64(0)
+        check(lib().escg_dev_band_rows(self._h, *[C.byref(x) for x in p], C.byref(nbytes)))
+        dev = torch.device("cuda", self.device)
+        return tuple(torch.as_tensor(_DevView(x.value, nbytes.value), device=dev) for x in p)
+
+    def advance(self, n_mcs: int):
+        import torch
+
+        k = self.info["kmcs"]
+        done = 0
+        while done < n_mcs:
+            chunk = min(k, n_mcs - done)
+            exchange_halos(*self.halo_views(), self.rank, self.world, self.group)
+            torch.cuda.synchronize(self.device)  # NCCL's stream → the engine's stream
+            check(lib().escg_dev_band_step(self._h, int(chunk)))
+            done += chunk

@@ -1217,6 +1217,67 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
     });
 }
 
+int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint8_t** send_bot, uint8_t** recv_bot,
+                       int64_t* bytes) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (h->nbands < 2) config_error("not a band engine");
+        uint8_t* base = h->lat[h->cur[0]].p;
+        const size_t row = static_cast<size_t>(h->L);
+        if (recv_top) *recv_top = base;
+        if (send_top) *send_top = base + static_cast<size_t>(h->halo) * row;
+        if (send_bot) *send_bot = base + static_cast<size_t>(h->band_rows) * row;
+        if (recv_bot) *recv_bot = base + static_cast<size_t>(h->halo + h->band_rows) * row;
+        if (bytes) *bytes = static_cast<int64_t>(h->halo) * h->L;
+    });
+}
+
+int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (h->nbands < 2) config_error("not a band engine");
+        if (n_mcs < 1 || n_mcs > h->kmcs)
+            config_error("band step must run 1.." + std::to_string(h->kmcs) + " MCS (the halo depth)");
+        CK(cudaSetDevice(h->device));
+        const int par = h->cur[0];
+        escgd::BlockArgs a{};
+        a.seeds = h->d_seeds.p;
+        a.rule = rule_args(h);
+        a.run = run_args(h, 0, 1, 0, 0, false);
+        a.H = h->H;
+        a.L = h->L;
+        a.S = h->S;
+        a.P = h->P;
+        a.arity = h->arity;
+        a.narrow = h->narrow;
+        a.Hg = h->Hg;
+        a.row0 = h->row0;
+        a.wrap_rows = h->wrap_rows;
+        a.reflect = 0;
+        a.seam_np = 0;
+        a.nby = h->nby;
+        a.nbx = h->nbx;
+        a.row_split = h->d_rows.p;
+        a.col_split = h->d_cols.p;
+        a.acc = h->d_acc.p;
+        a.ticket = h->d_ticket.p;
+        a.smem_bytes = h->smem;
+        a.step = 1;
+        a.count = 0;
+        a.src = h->lat[par].p;
+        a.dst = h->lat[1 - par].p;
+        a.dst_index = 1 - par;
+        a.mcs = h->mcs[0];
+        a.nmcs = n_mcs;
+        CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
+        CK(escgd::launch_block(a, 1, h->threads, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->cur[0] = 1 - par;
+        h->mcs[0] += n_mcs;
+        h->last_launches = 1;
+    });
+}
+
 int escg_dev_draw_format(escg_dev* h, int32_t* narrow) {
     return guarded([&] {
         if (!h || !narrow) config_error("null argument");

@@ -77,3 +77,48 @@ def test_sharded_ensemble_world2_equals_world1():
     assert [tuple(map(lambda x: tuple(x) if isinstance(x, list) else x, r)) for r in res2] == \
         [tuple(map(lambda x: tuple(x) if isinstance(x, list) else x, r)) for r in res1]
     assert m == 3.0
+
+
+def _halo_worker(rank, world, port, q, H, L, halo):
+    """Each rank holds halo + band + halo rows of a global lattice (as a band engine's buffer does);
+    after exchange_halos its halos must equal the global rows above/below the band (periodic)."""
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_16639_b200.bands import band_rows, exchange_halos
+
+    G = np.arange(H * L, dtype=np.int64).reshape(H, L) % 251
+    start, rows = band_rows(H, world)[rank]
+    buf = torch.full(((rows + 2 * halo) * L,), 255, dtype=torch.uint8)
+    buf[halo * L:(halo + rows) * L] = torch.from_numpy(G[start:start + rows].astype(np.uint8).ravel())
+    v = buf.view(rows + 2 * halo, L)
+    recv_top, send_top = v[:halo].reshape(-1), v[halo:2 * halo].reshape(-1)
+    send_bot, recv_bot = v[rows:rows + halo].reshape(-1), v[rows + halo:].reshape(-1)
+    exchange_halos(recv_top, send_top, send_bot, recv_bot, rank, world)
+    want_top = G[[(start - halo + i) % H for i in range(halo)]].astype(np.uint8)
+    want_bot = G[[(start + rows + i) % H for i in range(halo)]].astype(np.uint8)
+    ok = np.array_equal(v[:halo].numpy(), want_top) and np.array_equal(v[rows + halo:].numpy(), want_bot)
+    ok = ok and np.array_equal(v[halo:halo + rows].numpy(), G[start:start + rows].astype(np.uint8))
+    q.put((rank, bool(ok)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_band_halo_exchange_gloo(world):
+    """The multi-process band group's halo exchange (bands.exchange_halos, the NCCL path's host
+    logic) moves exactly the neighbours' edge rows, for world 2 (both neighbours the same rank) and 3."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    H, L, halo = 48, 20, 12
+    procs = [ctx.Process(target=_halo_worker, args=(r, world, port, q, H, L, halo)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert got == {r: True for r in range(world)}

@@ -447,3 +447,46 @@ def test_block_kernel_seams_match_crs_oracle(escg, oracle, LH, arity, kmcs, name
     want9 = oracle.crs_run(want, L, H, model.matrix(), M, 777, 5, 4, arity=arity)
     assert np.array_equal(final, want9)
     assert steps.tolist()[-1] == 9 and counts[-1].tolist() == np.bincount(want9, minlength=S + 1).tolist()
+
+
+@pytest.mark.parametrize("n_bands,kmcs", [(2, 2), (3, 1), (4, 3)])
+def test_band_primitives_match_single_lattice(escg, n_bands, kmcs):
+    """The multi-process band path in one process: halo rows moved between band buffers with torch
+    device copies (what NCCL send/recv does across ranks) through escg_dev_band_rows, then
+    escg_dev_band_step — equals the single-lattice run bit for bit."""
+    import torch
+
+    from paper_2508_16639_b200._lib import check, lib
+    from paper_2508_16639_b200.bands import DistributedBand
+
+    L, H = 96, 192
+    p = params(escg, L, H, 3, 1e-2, 0.1, 4, True, seed=31)
+    model = escg.make_circulant(3, [1])
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(11)
+        want = eng.get_lattice()
+    bands = [DistributedBand(p, model, rank=g, world=n_bands, device=0, kmcs=kmcs) for g in range(n_bands)]
+    try:
+        for b in bands:
+            s, r = b.info["start"], b.info["rows"]
+            b.set_band(init[s * L:(s + r) * L], 0)
+        done = 0
+        while done < 11:
+            chunk = min(kmcs, 11 - done)
+            views = [b.halo_views() for b in bands]
+            for g in range(n_bands):
+                up, dn = views[(g - 1) % n_bands], views[(g + 1) % n_bands]
+                views[g][0].copy_(up[2])  # top halo ← the band above's last rows
+                views[g][3].copy_(dn[1])  # bottom halo ← the band below's first rows
+            torch.cuda.synchronize()
+            for b in bands:
+                check(lib().escg_dev_band_step(b._h, chunk))
+            done += chunk
+        got = np.concatenate([b.get_band() for b in bands])
+        assert np.array_equal(got, want)
+        assert sum(b.counts() for b in bands).tolist() == np.bincount(want, minlength=4).tolist()
+    finally:
+        for b in bands:
+            b.close()
