@@ -747,11 +747,13 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         }
         h->kernel = choice;
         // NARROW (16-bit attempt words, one draw per tile pair) when migrations dominate so much that
-        // at most 1/64 of attempts leave the coarse fast path; needs periodic wrap and L % 8 == 0.
+        // at most 1/300 of attempts leave the coarse fast path (measured on B200: L=1000, M=1e-4 has
+        // 1/100 slow and runs 24% faster WIDE; L=2000 ≈ 1/370 is even; L=3200 ≈ 1/800 is 17% faster
+        // NARROW); needs periodic wrap with L, H ≡ 0 (mod 4) and L % 8 == 0.
         {
             const int LB = h->arity == 8 ? 5 : 4, CB = 16 - LB;
             const uint64_t fast_coarse = h->th.xm >> (32 - CB);
-            h->narrow = (periodic4 && h->L % 8 == 0 && fast_coarse * 64 >= 63ull * (1ull << CB)) ? 1 : 0;
+            h->narrow = (periodic4 && h->L % 8 == 0 && fast_coarse * 300 >= 299ull * (1ull << CB)) ? 1 : 0;
             if (const char* f = std::getenv("ESCG_DRAW_FORMAT")) {
                 if (std::strcmp(f, "wide") == 0) h->narrow = 0;
                 if (std::strcmp(f, "narrow") == 0 && periodic4 && h->L % 8 == 0) h->narrow = 1;
