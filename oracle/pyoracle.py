@@ -296,3 +296,8 @@ class Reference:
         a = np.ascontiguousarray(a, np.float64)
         b = np.ascontiguousarray(b, np.float64)
         return float(self.lib.ref_ks_two_sample_pvalue(a, a.size, b, b.size))
+
+    def chi_square_uniform(self, bins):
+        """stats.cpp chi_square_uniform_pvalue (the reference's own uniformity test)."""
+        b = np.ascontiguousarray(bins, np.uint64)
+        return float(self.lib.ref_chi_square_uniform_pvalue(b, b.size))

@@ -490,3 +490,39 @@ def test_band_primitives_match_single_lattice(escg, n_bands, kmcs):
     finally:
         for b in bands:
             b.close()
+
+
+@pytest.mark.parametrize("L,H,flux,arity,kernel,fmt", [(64, 64, True, 4, "tile", "narrow"), (48, 40, True, 8, "tile", "wide"),
+                                                       (1024, 512, True, 4, "block", "narrow"),
+                                                       (1000, 520, True, 4, "block", "wide"),
+                                                       (501, 463, True, 8, "block", "wide"),
+                                                       (333, 200, False, 4, "block", "wide"),
+                                                       (51, 45, True, 4, "tile", "wide")])
+def test_pure_exchange_conserves_every_species(escg, L, H, flux, arity, kernel, fmt, monkeypatch):
+    """SURVEY §4.3 (criteria 3/11): with no predation (D = 0) and no empty cells only exchanges can
+    fire, so every species count is conserved exactly — the invariant the reference's racy
+    parallel engines violate.  Covers every kernel mode (periodic NARROW/WIDE, seams, reflect)."""
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", fmt)
+    D = escg.DominanceModel(3, escg.DominanceModel.Kind.Binary, np.zeros(9))
+    p = params(escg, L, H, 3, 1e-1, 0.0, arity, flux, seed=5)
+    with escg.DeviceEngine(p, D, kernel=kernel) as eng:
+        eng.init_lattice()
+        c0 = eng.counts()
+        init = eng.get_lattice()
+        eng.advance(40)
+        assert eng.counts().tolist() == c0.tolist()
+        assert not np.array_equal(eng.get_lattice(), init)
+        assert c0[0] == 0
+
+
+def test_device_init_lattice_is_uniform(escg, ref):
+    """SURVEY §4.3 criterion 12: device init_lattice species frequencies pass the reference's own
+    chi-square uniformity test (stats.cpp chi_square_uniform_pvalue) and the empty fraction matches."""
+    L = 2048
+    p = params(escg, L, L, 5, 1e-4, 0.2, 4, True, seed=12345)
+    with escg.DeviceEngine(p, escg.make_rpsls(), kernel="block") as eng:
+        eng.init_lattice()
+        c = eng.counts()
+    n = L * L
+    assert abs(c[0] / n - 0.2) < 5 * np.sqrt(0.2 * 0.8 / n)
+    assert ref.chi_square_uniform(c[1:]) > 1e-3
