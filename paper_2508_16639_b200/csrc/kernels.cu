@@ -165,7 +165,7 @@ __device__ void block_count(const uint8_t* base, int rows, int cols, int pitch, 
 // ---------------------------------------------------------------------------------------------
 
 struct TileSmem {
-    int lat_bytes, T_off, snap_off, cnt_off, flag_off, tbl_off, total;
+    int lat_bytes, T_off, snap_off, cnt_off, flag_off, total;
 };
 
 __host__ __device__ inline TileSmem tile_layout(int H, int L, int S, int P) {
@@ -176,8 +176,7 @@ __host__ __device__ inline TileSmem tile_layout(int H, int L, int S, int P) {
     t.snap_off = t.T_off + align16(S1 * S1 * 4);
     t.cnt_off = t.snap_off + align16(3 * (L + 3) + 3 * H);
     t.flag_off = t.cnt_off + align16((kMaxSpecies + 1) * 4);
-    t.tbl_off = t.flag_off + 16;
-    t.total = t.tbl_off + 32 * 8;
+    t.total = t.flag_off + 16;
     return t;
 }
 
@@ -243,7 +242,7 @@ constexpr int kModePeriodic = 0, kModeReflect = 1, kModeSeam = 2;
 
 // One MCS of the seam mode: 4, 6 or 9 phases of single WIDE tiles.
 template <int ARITY>
-__device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t tbl, uint32_t sT,
+__device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap,
                                 const RuleArgs& rule, int H, int L, int P, int S1, uint32_t s32, uint64_t mcs) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const SeamAxis ay(H), ax(L);
@@ -273,11 +272,11 @@ __device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint
 
 // One MCS of the tile kernel (whole lattice in shared memory at lat0, ghost frame when periodic).
 template <int ARITY, int MODE>
-__device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap, uint32_t tbl, uint32_t sT,
+__device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap,
                            const RuleArgs& rule, int narrow, int H, int L, int P, int S1, uint32_t s32,
                            uint64_t mcs) {
     if (MODE == kModeSeam) {
-        tile_round_seam<ARITY>(lat0, lat, snap, tbl, sT, rule, H, L, P, S1, s32, mcs);
+        tile_round_seam<ARITY>(lat0, lat, snap, rule, H, L, P, S1, s32, mcs);
         return;
     }
     constexpr bool REFLECT = MODE == kModeReflect;
@@ -373,7 +372,7 @@ __device__ void tile_copy(uint8_t* lat, uint8_t* glat, int H, int L, int P) {
 template <int ARITY, int MODE>
 __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     constexpr bool REFLECT = MODE == kModeReflect;
-    extern __shared__ __align__(16) uint8_t smem[];
+    extern __shared__ __align__(128) uint8_t smem[];
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
     const TileSmem lay = tile_layout(H, L, a.S, P);
     uint8_t* lat = smem;
@@ -381,7 +380,6 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     uint8_t* snap = smem + lay.snap_off;
     uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + lay.cnt_off);
     int* sFlag = reinterpret_cast<int*>(smem + lay.flag_off);
-    int2* tblp = reinterpret_cast<int2*>(smem + lay.tbl_off);
     const int tid = threadIdx.x, nt = blockDim.x;
     const int r = blockIdx.x;
     uint8_t* glat = a.lat + static_cast<size_t>(r) * H * L;
@@ -395,7 +393,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
         ghost_pass<false>(lat, snap, H, L, P);
         __syncthreads();
     }
-    const uint32_t lat0 = smem_addr(lat), tbl = smem_addr(tblp), sTa = smem_addr(sT);
+    const uint32_t lat0 = smem_addr(lat);
     int64_t mcs = a.run.mcs[r];
     int status = a.run.status[r];
     for (;;) {
@@ -419,7 +417,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
             adv = a.run.mcs_limit - mcs;
         }
         for (int64_t k = 0; k < adv; ++k, ++mcs)
-            tile_round<ARITY, MODE>(lat0, lat, snap, tbl, sTa, a.rule, a.narrow, H, L, P, S1, s32,
+            tile_round<ARITY, MODE>(lat0, lat, snap, a.rule, a.narrow, H, L, P, S1, s32,
                                        static_cast<uint64_t>(mcs));
     }
     tile_copy<false>(lat, glat, H, L, P);
@@ -446,8 +444,8 @@ struct BlockGeom {
 };
 
 template <int ARITY, bool NARROW>
-__device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs rule, uint32_t win0, uint32_t tbl,
-                                             uint32_t sT, int S1, int Wh, int Ww, int wy0, int wx0, uint32_t s32) {
+__device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs rule, uint32_t win0, int Wh, int Ww,
+                                             int wy0, int wx0, uint32_t s32) {
     const int tid = threadIdx.x, nt = blockDim.x, P = g.P;
     const int Ty = g.Hg >> 1, Tx = g.L >> 1, TQ = g.L >> 3;
     // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
@@ -858,8 +856,8 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     uint8_t* win = smem;
     const int woff = (Wh * P + 15) & ~15;
     uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
-    int2* tblp = reinterpret_cast<int2*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15));
-    uint32_t* sCnt = reinterpret_cast<uint32_t*>(tblp + 32);
+    // (256 bytes after the thresholds are reserved: block_smem's layout predates the static tables)
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8);
     uint8_t* sScratch = reinterpret_cast<uint8_t*>(sCnt + kMaxSpecies + 1);  // 4 * P bytes (dummy box)
     __shared__ int sLast;
     __shared__ __align__(8) uint64_t sMbar;
@@ -930,7 +928,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
 #endif
         __syncthreads();
         DIAG_STAMP(2);
-        const uint32_t win0 = smem_addr(win), tbl = smem_addr(tblp), sTa = smem_addr(sT);
+        const uint32_t win0 = smem_addr(win);
         BlockGeom g;
         g.P = P;
         g.H = H;
@@ -941,9 +939,9 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         g.mcs = a.mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, true>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) {
             // generic-proxy writes → async proxy, then one bulk store per block row
@@ -1018,11 +1016,10 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
     const int Whm = bh + 2 * My;
     const int woff = (Whm * P + 15) & ~15;
     uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
-    int2* tblp = reinterpret_cast<int2*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15));
-    uint32_t* sCnt = reinterpret_cast<uint32_t*>(tblp + 32);
+    // (256 bytes after the thresholds are reserved: block_smem's layout predates the static tables)
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8);
     uint8_t* sScratch = reinterpret_cast<uint8_t*>(sCnt + kMaxSpecies + 1);
     __shared__ __align__(8) uint64_t sMbar;
-    const int nblk = gridDim.x * gridDim.y;  // CTAs per replica
 
     const uint32_t s32 = seed32(a.seeds[r]);
     for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
@@ -1034,7 +1031,7 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const uint32_t win0 = smem_addr(win), tbl = smem_addr(tblp), sTa = smem_addr(sT);
+    const uint32_t win0 = smem_addr(win);
     const RunArgs& run = a.run;
     const int64_t limit = pa.record ? run.mcs_limit : pa.mcs_end;
     int64_t mcs = pa.mcs0;
@@ -1104,9 +1101,9 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
         g.mcs = mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, true>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false>(g, a.rule, win0, tbl, sTa, S1, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         store_block<16>(dst, win, L, P, bh, bw, ry0, rx0, Myc, Mxc);
         mcs += chunk;
         par ^= 1;
