@@ -99,7 +99,8 @@ def run_reference_arm(args):
             vals.append(v)
             times.append(el)
     value = L * L * 10 * len(times) / sum(times)
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "device": "host CPU (no GPU used)",
+            "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": value / PUBLISHED_ATTEMPTS_PER_S, "dtype": "int32", "data": "synthetic",
             "impl": "reference", "mcs_per_s": value / (L * L),
