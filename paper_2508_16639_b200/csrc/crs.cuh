@@ -195,6 +195,7 @@ __device__ __forceinline__ uint2 offsets(uint32_t bits) {
 struct PhaseCtx {
     uint32_t fast;       // attempt bits below this are certain migrations (NARROW fast path)
     uint32_t xm, xi;     // X_mig, X_int (WIDE rule)
+    uint32_t bf;         // WIDE rule form: 1 branch-free (mixed actions), 0 branchy (migration-dominated)
     uint32_t c1, c2, c3;  // draw counter words
 };
 constexpr uint32_t kStepToRefine = (0u ^ 1u) << 16;  // kDomStep ^ kDomRefine in the domain field
@@ -273,34 +274,63 @@ __device__ __noinline__ uint32_t slow_narrow(uint32_t s, uint32_t n, uint32_t ha
     return rule_exact_s(s, n, x, sSlow.xm, sSlow.xi, sSlow.sT, sSlow.S1);
 }
 
+// 32-bit shared load under a predicate (no branch); `dflt` when the predicate is false.
+__device__ __forceinline__ uint32_t lds32_if(bool p, uint32_t a, uint32_t dflt) {
+    uint32_t v = dflt;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+        : "+r"(v)
+        : "r"(a), "r"(static_cast<uint32_t>(p)));
+    return v;
+}
+
 // WIDE rule on the coarse word (low LB bits zero).  A comparison against threshold T is decided by
-// the coarse bits unless coarse == T >> LB; those (rare) words take the exact path.
+// the coarse bits unless coarse == T >> LB; those (rare) words take the exact path.  Branch-free:
+// the migration / reproduction / interaction outcomes are selects and the interaction thresholds
+// predicated loads, so lanes with different actions do not serialise (mixed buckets are the norm
+// when P(migration) is 0.8-0.99); only the exact path branches.
 template <int ARITY>
 __device__ __forceinline__ uint32_t rule_wide(uint32_t s, uint32_t n, uint32_t word, uint32_t tile, int a,
                                               const PhaseCtx& C) {
     constexpr uint32_t HI = ~((1u << Bits<ARITY>::LB) - 1u);
     const uint32_t x = word & HI;
-    bool exact = (x == (C.xm & HI)) | (x == (C.xi & HI));
-    uint32_t ns = s, nn = n;
-    if (!exact) {
-        if (x < C.xm) {
-            ns = n;
-            nn = s;
-        } else if (x >= C.xi) {
-            if (n == 0u)
-                nn = s;
-            else if (s == 0u)
+    if (!C.bf) {
+        // branchy form: when migrations dominate (P >= 0.97) whole warps take the first branch and
+        // never issue the interaction loads
+        bool exact = (x == (C.xm & HI)) | (x == (C.xi & HI));
+        uint32_t ns = s, nn = n;
+        if (!exact) {
+            if (x < C.xm) {
                 ns = n;
-        } else if ((s != 0u) & (n != 0u) & (s != n)) {
-            const uint32_t sT = sSlow.sT, S1 = static_cast<uint32_t>(sSlow.S1);
-            const uint32_t t1 = lds32(sT + 4u * (s * S1 + n)), t2 = lds32(sT + 4u * (n * S1 + s));
-            exact = (x == (t1 & HI)) | (x == (t2 & HI));
-            if (x < t1)
-                nn = 0u;
-            else if (x < t2)
-                ns = 0u;
+                nn = s;
+            } else if (x >= C.xi) {
+                if (n == 0u)
+                    nn = s;
+                else if (s == 0u)
+                    ns = n;
+            } else if ((s != 0u) & (n != 0u) & (s != n)) {
+                const uint32_t sT = sSlow.sT, S1 = static_cast<uint32_t>(sSlow.S1);
+                const uint32_t t1 = lds32(sT + 4u * (s * S1 + n)), t2 = lds32(sT + 4u * (n * S1 + s));
+                exact = (x == (t1 & HI)) | (x == (t2 & HI));
+                if (x < t1)
+                    nn = 0u;
+                else if (x < t2)
+                    ns = 0u;
+            }
         }
+        if (exact) return slow_wide<ARITY>(s, n, word, tile, a, C.c1, C.c2, C.c3);
+        return ns | (nn << 8);
     }
+    const bool mig = x < C.xm, rep = x >= C.xi;
+    const bool inter = !mig & !rep & (s != 0u) & (n != 0u) & (s != n);
+    const uint32_t sT = sSlow.sT, S1 = static_cast<uint32_t>(sSlow.S1);
+    const uint32_t t1 = lds32_if(inter, sT + 4u * (s * S1 + n), 0u);
+    const uint32_t t2 = lds32_if(inter, sT + 4u * (n * S1 + s), 0u);
+    const bool exact = (x == (C.xm & HI)) | (x == (C.xi & HI)) | (inter & ((x == (t1 & HI)) | (x == (t2 & HI))));
+    const bool k1 = inter & (x < t1);               // u < D[s][n]: the neighbour dies
+    const bool k2 = inter & !(x < t1) & (x < t2);   // else u < D[n][s]: the cell dies
+    const bool r1 = rep & (n == 0u), r2 = rep & (n != 0u) & (s == 0u);
+    const uint32_t ns = mig ? n : (k2 ? 0u : (r2 ? n : s));
+    const uint32_t nn = mig ? s : (k1 ? 0u : (r1 ? s : n));
     if (exact) return slow_wide<ARITY>(s, n, word, tile, a, C.c1, C.c2, C.c3);
     return ns | (nn << 8);
 }

@@ -306,7 +306,13 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
 
 escgd::RuleArgs rule_args(escg_dev* h) {
     const int LB = h->arity == 8 ? 5 : 4;
-    return escgd::RuleArgs{h->th.xm, h->th.xi, h->d_T.p, (h->th.xm >> (16 + LB)) << LB};
+    // WIDE rule form (crs.cuh rule_wide, a kernel template parameter): branch-free unless
+    // migrations dominate so much that whole warps usually take the migration branch (measured
+    // crossovers: block kernel between P(migration) 0.968 and 0.990, tile kernel between 0.941 and
+    // 0.976 — tools/wide_rule_sweep.py; branch-free is 23% faster at 0.8, branchy 27% at 0.99)
+    uint32_t bf = static_cast<double>(h->th.xm) < 0.97 * 4294967296.0 ? 1u : 0u;
+    if (const char* f = std::getenv("ESCG_WIDE_RULE")) bf = std::strcmp(f, "branchy") == 0 ? 0u : 1u;
+    return escgd::RuleArgs{h->th.xm, h->th.xi, h->d_T.p, (h->th.xm >> (16 + LB)) << LB, bf};
 }
 
 escgd::RunArgs run_args(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int tracked, bool trace) {

@@ -211,7 +211,7 @@ __device__ void ghost_pass(uint8_t* lat, uint8_t* snap, int H, int L, int P) {
     }
 }
 
-template <int ARITY>
+template <int ARITY, bool BF = false>
 __device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, uint64_t mcs, int p, uint32_t s32) {
     constexpr int LB = Bits<ARITY>::LB;
     PhaseCtx C;
@@ -219,6 +219,7 @@ __device__ __forceinline__ PhaseCtx phase_ctx(const RuleArgs& rule, int narrow, 
     C.fast = narrow ? rule.fast : 0u;
     C.xm = rule.xm;
     C.xi = rule.xi;
+    C.bf = BF ? 1u : 0u;  // compile-time: the other rule_wide form folds away
     C.c1 = static_cast<uint32_t>(mcs);
     C.c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
     C.c3 = s32;
@@ -241,7 +242,7 @@ __device__ __forceinline__ void attempt_setup(const RuleArgs& rule, uint32_t sT,
 constexpr int kModePeriodic = 0, kModeReflect = 1, kModeSeam = 2;
 
 // One MCS of the seam mode: 4, 6 or 9 phases of single WIDE tiles.
-template <int ARITY>
+template <int ARITY, bool BF>
 __device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap,
                                 const RuleArgs& rule, int H, int L, int P, int S1, uint32_t s32, uint64_t mcs) {
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -251,7 +252,7 @@ __device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap,
 #pragma unroll 1
     for (int p = 0; p < np; ++p) {
         const int v = rg.colour(p), cy = v / ax.nc, cx = v - cy * ax.nc;
-        const PhaseCtx C = phase_ctx<ARITY>(rule, 0, mcs, p, s32);
+        const PhaseCtx C = phase_ctx<ARITY, BF>(rule, 0, mcs, p, s32);
         const uint32_t c2 = C.c2;
         const int nty = ay.count(cy), ntx = ax.count(cx), cnt = nty * ntx;
         for (int k = tid; k < cnt; k += nt) {
@@ -271,12 +272,12 @@ __device__ void tile_round_seam(uint32_t lat0, uint8_t* lat, uint8_t* snap,
 }
 
 // One MCS of the tile kernel (whole lattice in shared memory at lat0, ghost frame when periodic).
-template <int ARITY, int MODE>
+template <int ARITY, int MODE, bool BF>
 __device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap,
                            const RuleArgs& rule, int narrow, int H, int L, int P, int S1, uint32_t s32,
                            uint64_t mcs) {
     if (MODE == kModeSeam) {
-        tile_round_seam<ARITY>(lat0, lat, snap, rule, H, L, P, S1, s32, mcs);
+        tile_round_seam<ARITY, BF>(lat0, lat, snap, rule, H, L, P, S1, s32, mcs);
         return;
     }
     constexpr bool REFLECT = MODE == kModeReflect;
@@ -287,7 +288,7 @@ __device__ void tile_round(uint32_t lat0, uint8_t* lat, uint8_t* snap,
 #pragma unroll 1
     for (int p = 0; p < 4; ++p) {
         const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-        const PhaseCtx C = phase_ctx<ARITY>(rule, narrow, mcs, p, s32);
+        const PhaseCtx C = phase_ctx<ARITY, BF>(rule, narrow, mcs, p, s32);
         const uint32_t c2 = C.c2;
         const int nty = (Ty - cy + 1) >> 1;
         const int ntx = (Tx - cx + 1) >> 1;  // tiles of this colour per tile row
@@ -369,7 +370,7 @@ __device__ void tile_copy(uint8_t* lat, uint8_t* glat, int H, int L, int P) {
     }
 }
 
-template <int ARITY, int MODE>
+template <int ARITY, int MODE, bool BF>
 __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     constexpr bool REFLECT = MODE == kModeReflect;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
             adv = a.run.mcs_limit - mcs;
         }
         for (int64_t k = 0; k < adv; ++k, ++mcs)
-            tile_round<ARITY, MODE>(lat0, lat, snap, a.rule, a.narrow, H, L, P, S1, s32,
+            tile_round<ARITY, MODE, BF>(lat0, lat, snap, a.rule, a.narrow, H, L, P, S1, s32,
                                        static_cast<uint64_t>(mcs));
     }
     tile_copy<false>(lat, glat, H, L, P);
@@ -443,7 +444,7 @@ struct BlockGeom {
     uint32_t scratch;  // smem address of a dummy 4-row box (edge items with one invalid tile)
 };
 
-template <int ARITY, bool NARROW>
+template <int ARITY, bool NARROW, bool BF>
 __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs rule, uint32_t win0, int Wh, int Ww,
                                              int wy0, int wx0, uint32_t s32) {
     const int tid = threadIdx.x, nt = blockDim.x, P = g.P;
@@ -460,7 +461,7 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
         for (int p = 0; p < 4; ++p) {
             const int q = 4 * t + p;  // global phase of this launch: validity shrinks 3 cells per phase
             const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-            const PhaseCtx C = phase_ctx<ARITY>(rule, NARROW, mcs, p, s32);
+            const PhaseCtx C = phase_ctx<ARITY, BF>(rule, NARROW, mcs, p, s32);
             const uint32_t c2 = C.c2;
             // footprint rows [2j-oy-1, 2j-oy+2] within [3q, Wh-3q); cols within [ex+3q, Ww-ex-3q)
             const int lo = 3 * q, hiR = Wh - 3 * q, loC = ex + 3 * q, hiC = Ww - ex - 3 * q;
@@ -669,7 +670,7 @@ __device__ __forceinline__ void store_block(uint8_t* dst, const uint8_t* win, in
 // follow the reflect tiling of orc_crs_run (T = (n + o + 1) / 2 per axis, partial edge tiles), WIDE
 // draws.  Pairs whose footprints stay inside the lattice take the fast dual path; pairs touching the
 // mirror go through tile_reflect (explicit coordinates, reflected neighbours, skipped cells).
-template <int ARITY>
+template <int ARITY, bool BF>
 __device__ void block_phases_reflect(const RuleArgs& rule, uint32_t win0, int H, int L, int P, int nmcs,
                                      int64_t mcs0, int Wh, int Ww, int wy0, int wx0, int ex, uint32_t s32) {
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -684,7 +685,7 @@ __device__ void block_phases_reflect(const RuleArgs& rule, uint32_t win0, int H,
         for (int p = 0; p < 4; ++p) {
             const int q = 4 * t + p;
             const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
-            const PhaseCtx C = phase_ctx<ARITY>(rule, 0, mcs, p, s32);
+            const PhaseCtx C = phase_ctx<ARITY, BF>(rule, 0, mcs, p, s32);
             const int jlo = top ? 0 : ((3 * q + rp.oy + 2) >> 1);
             const int jhi = bot ? (Ty - 1 - jb) : ((Wh - 3 * q - 3 + rp.oy) >> 1);
             const int ilo = lft ? 0 : ((ex + 3 * q + rp.ox + 2) >> 1);
@@ -788,7 +789,7 @@ __device__ void seam_axis_lists(SeamEntry* lists, int* counts, int W, int w0, in
         for (int c = 0; c < 3; ++c) counts[c] = min(cnt[c], cap);
 }
 
-template <int ARITY>
+template <int ARITY, bool BF>
 __device__ void block_phases_seam(const RuleArgs& rule, uint32_t win0, int H, int L, int P, int nmcs, int64_t mcs0,
                                   int Wh, int Ww, int wy0, int wx0, uint32_t s32, SeamEntry* rows, SeamEntry* cols,
                                   int* counts) {
@@ -806,7 +807,7 @@ __device__ void block_phases_seam(const RuleArgs& rule, uint32_t win0, int H, in
         for (int p = 0; p < np; ++p) {
             const int q = np * t + p;
             const int v = rg.colour(p), cy = v / ax.nc, cx = v - cy * ax.nc;
-            const PhaseCtx C = phase_ctx<ARITY>(rule, 0, mcs, p, s32);
+            const PhaseCtx C = phase_ctx<ARITY, BF>(rule, 0, mcs, p, s32);
             const int ny = counts[cy], nx = counts[3 + cx], cnt = ny * nx;
             const int lo = 3 * q, hiY = Wh - 3 * q, hiX = Ww - 3 * q;
             for (int k = tid; k < cnt; k += nt) {
@@ -835,7 +836,7 @@ __device__ void load_window_bytes(uint8_t* win, const uint8_t* src, int H, int L
     }
 }
 
-template <int ARITY, int BMODE>
+template <int ARITY, int BMODE, bool BF>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     constexpr bool REFLECT = BMODE == 1, SEAM = BMODE == 2;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -880,7 +881,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
         load_window_bytes(win, src, H, L, P, Wh, Ww, wy0, wx0);
         __syncthreads();
-        block_phases_seam<ARITY>(a.rule, smem_addr(win), H, L, P, a.nmcs, a.mcs, Wh, Ww, wy0, wx0, s32, rows, cols,
+        block_phases_seam<ARITY, BF>(a.rule, smem_addr(win), H, L, P, a.nmcs, a.mcs, Wh, Ww, wy0, wx0, s32, rows, cols,
                                  sSeamCnt);
         copy_region<false>(win + My * P + Mx, P, dst + static_cast<size_t>(ry0) * L + rx0, L, bh, bw);
     } else if (REFLECT && a.step) {
@@ -893,7 +894,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
         copy_region<true>(win, P, const_cast<uint8_t*>(src) + static_cast<size_t>(wy0) * L + wx0, L, wh, ww);
         __syncthreads();
-        block_phases_reflect<ARITY>(a.rule, smem_addr(win), H, L, P, a.nmcs, a.mcs, wh, ww, wy0, wx0, Mx - My, s32);
+        block_phases_reflect<ARITY, BF>(a.rule, smem_addr(win), H, L, P, a.nmcs, a.mcs, wh, ww, wy0, wx0, Mx - My, s32);
         copy_region<false>(win + (ry0 - wy0) * P + (rx0 - wx0), P, dst + static_cast<size_t>(ry0) * L + rx0, L, bh, bw);
     } else if (a.step) {
         const uint32_t s32 = seed32(a.seeds[r]);
@@ -939,9 +940,9 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         g.mcs = a.mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, true, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, false, BF>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) {
             // generic-proxy writes → async proxy, then one bulk store per block row
@@ -1101,9 +1102,9 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
         g.mcs = mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, true, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases<ARITY, false, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         store_block<16>(dst, win, L, P, bh, bw, ry0, rx0, Myc, Mxc);
         mcs += chunk;
         par ^= 1;
@@ -1280,7 +1281,7 @@ cudaError_t launch_count(const uint8_t* lat, int64_t n, int nrep, int S, unsigne
 
 template <int ARITY, int MODE>
 static cudaError_t tile_launch_t(const TileArgs& a, int nrep, int threads, cudaStream_t s) {
-    auto k = tile_kernel<ARITY, MODE>;
+    auto k = a.rule.wide_bf ? tile_kernel<ARITY, MODE, true> : tile_kernel<ARITY, MODE, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<nrep, threads, a.smem_bytes, s>>>(a);
@@ -1301,10 +1302,13 @@ cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s
 
 template <int ARITY, int BMODE>
 static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cudaStream_t s) {
+    // NARROW launches never consult the WIDE rule: one instantiation
+    const bool bf = a.rule.wide_bf && !a.narrow;
     // the dynamic-smem opt-in is a per-device function attribute: remember it per device (band
     // groups drive several devices from one thread); atomics keep concurrent host threads safe
-    static std::atomic<int> configured_bytes[kMaxDevices];
-    auto k = block_kernel<ARITY, BMODE>;
+    static std::atomic<int> configured[2][kMaxDevices];  // [rule form][device]
+    std::atomic<int>* configured_bytes = configured[bf ? 1 : 0];
+    auto k = bf ? block_kernel<ARITY, BMODE, true> : block_kernel<ARITY, BMODE, false>;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

@@ -24,6 +24,7 @@ struct RuleArgs {
     uint32_t xm, xi;       // X_mig, X_int
     const uint32_t* T;     // (S+1)^2 interaction thresholds (device)
     uint32_t fast;         // NARROW certain-migration bound on attempt bits: (xm >> (16+LB)) << LB
+    uint32_t wide_bf;      // WIDE rule form: 1 branch-free (P(migration) < 0.97), 0 branchy
 };
 
 // Per-replica run bookkeeping (device arrays, length n_replicas unless noted).
