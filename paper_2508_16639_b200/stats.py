@@ -1,0 +1,109 @@
+"""Statistics helpers of the reference library (include/escg/stats.hpp, src/stats.cpp), used by the
+experiments harness and by the acceptance criteria the reference's SPEC states.
+
+    mean_std(xs)                     stats.cpp:9-21   sample mean and (n-1) standard deviation
+    gamma_q(a, x)                    stats.cpp:61-66  regularized upper incomplete gamma Q(a, x)
+    chi_square_uniform_pvalue(bins)  stats.cpp:68-81  P(chi2 >= observed) for equiprobable bins
+    ks_two_sample_pvalue(a, b)       stats.cpp:83-110 asymptotic two-sample Kolmogorov-Smirnov p
+
+Invalid arguments raise ValueError (the reference's std::invalid_argument).
+"""
+from __future__ import annotations
+
+import math
+from typing import Sequence
+
+from .experiments import MeanStd, mean_std  # noqa: F401  (stats.cpp:9-21 lives with the harness)
+
+_EPS = 1e-15
+_TINY = 1e-300
+
+
+def _log_prefactor(a: float, x: float) -> float:
+    return -x + a * math.log(x) - math.lgamma(a)
+
+
+def _gamma_p_series(a: float, x: float) -> float:
+    """P(a, x) = x^a e^-x / Gamma(a) * sum_k x^k / (a (a+1) ... (a+k)); for x < a + 1."""
+    term = 1.0 / a
+    total = term
+    denom = a
+    for _ in range(500):
+        denom += 1.0
+        term *= x / denom
+        total += term
+        if abs(term) < abs(total) * _EPS:
+            break
+    return total * math.exp(_log_prefactor(a, x))
+
+
+def _gamma_q_continued_fraction(a: float, x: float) -> float:
+    """Q(a, x) by the modified Lentz evaluation of its continued fraction; for x >= a + 1."""
+    b = x + 1.0 - a
+    c = 1.0 / _TINY
+    d = 1.0 / b
+    h = d
+    for i in range(1, 500):
+        an = -i * (i - a)
+        b += 2.0
+        d = an * d + b
+        if abs(d) < _TINY:
+            d = _TINY
+        c = b + an / c
+        if abs(c) < _TINY:
+            c = _TINY
+        d = 1.0 / d
+        delta = d * c
+        h *= delta
+        if abs(delta - 1.0) < _EPS:
+            break
+    return h * math.exp(_log_prefactor(a, x))
+
+
+def gamma_q(a: float, x: float) -> float:
+    if a <= 0.0 or x < 0.0:
+        raise ValueError("gamma_q requires a > 0 and x >= 0")
+    if x == 0.0:
+        return 1.0
+    if x < a + 1.0:
+        return 1.0 - _gamma_p_series(a, x)
+    return _gamma_q_continued_fraction(a, x)
+
+
+def chi_square_uniform_pvalue(bin_counts: Sequence[int]) -> float:
+    counts = [int(c) for c in bin_counts]
+    if len(counts) < 2:
+        raise ValueError("need at least two bins")
+    total = sum(counts)
+    if total == 0:
+        raise ValueError("need at least one sample")
+    expected = total / len(counts)
+    chi2 = sum((c - expected) ** 2 / expected for c in counts)
+    return gamma_q((len(counts) - 1) / 2.0, chi2 / 2.0)
+
+
+def ks_two_sample_pvalue(a: Sequence[float], b: Sequence[float]) -> float:
+    if len(a) == 0 or len(b) == 0:
+        raise ValueError("KS test needs non-empty samples")
+    xa, xb = sorted(float(v) for v in a), sorted(float(v) for v in b)
+    na, nb = len(xa), len(xb)
+    # sup |F_a - F_b| over the pooled sample points (ties advance both empirical CDFs together)
+    d, i, j = 0.0, 0, 0
+    while i < na and j < nb:
+        x = min(xa[i], xb[j])
+        while i < na and xa[i] <= x:
+            i += 1
+        while j < nb and xb[j] <= x:
+            j += 1
+        d = max(d, abs(i / na - j / nb))
+    ne = na * nb / (na + nb)
+    lam = (math.sqrt(ne) + 0.12 + 0.11 / math.sqrt(ne)) * d
+    # Kolmogorov survival function Q_KS(lambda) = 2 sum_k (-1)^(k-1) exp(-2 k^2 lambda^2)
+    p, sign = 0.0, 1.0
+    for k in range(1, 101):
+        term = math.exp(-2.0 * k * k * lam * lam)
+        p += 2.0 * sign * term
+        sign = -sign
+        if term < 1e-12:
+            break
+    return min(1.0, max(0.0, p))

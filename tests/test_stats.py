@@ -1,0 +1,49 @@
+"""stats.py (the reference's stats.cpp mirrored) against the compiled reference through the shim."""
+import numpy as np
+import pytest
+
+
+def test_stats_match_reference(ref):
+    from paper_2508_16639_b200 import stats as S
+
+    rng = np.random.default_rng(4)
+    for _ in range(200):
+        k = int(rng.integers(2, 40))
+        bins = rng.integers(0, 1000, size=k).astype(np.uint64)
+        if bins.sum() == 0:
+            continue
+        want = ref.chi_square_uniform(bins)
+        assert S.chi_square_uniform_pvalue(bins.tolist()) == pytest.approx(want, rel=1e-12, abs=1e-300)
+    for _ in range(200):
+        a = rng.normal(0, 1, int(rng.integers(1, 300)))
+        b = rng.normal(rng.uniform(-0.5, 0.5), 1, int(rng.integers(1, 300)))
+        if rng.random() < 0.3:  # ties
+            a, b = np.round(a, 1), np.round(b, 1)
+        assert S.ks_two_sample_pvalue(a, b) == pytest.approx(ref.ks(a, b), rel=1e-12, abs=1e-15)
+
+
+def test_stats_edges():
+    from paper_2508_16639_b200 import stats as S
+
+    assert S.gamma_q(1.0, 0.0) == 1.0
+    assert S.gamma_q(1.0, 2.0) == pytest.approx(np.exp(-2.0), rel=1e-13)  # Q(1, x) = e^-x
+    assert S.gamma_q(2.5, 1.0) + (1 - S.gamma_q(2.5, 1.0)) == 1.0
+    assert S.chi_square_uniform_pvalue([10, 10, 10]) == 1.0
+    # identical samples: lambda = 0, the reference's 100-term alternating series sums to 0 (a quirk
+    # of stats.cpp:99-108 kept for parity; tests/test_stats.py::test_ks_identical_samples_as_reference)
+    assert S.ks_two_sample_pvalue([1, 2, 3], [1, 2, 3]) == 0.0
+    for bad in ([5], [0, 0]):
+        with pytest.raises(ValueError):
+            S.chi_square_uniform_pvalue(bad)
+    with pytest.raises(ValueError):
+        S.ks_two_sample_pvalue([], [1.0])
+    with pytest.raises(ValueError):
+        S.gamma_q(0.0, 1.0)
+    m = S.mean_std([2.0, 4.0])
+    assert (m.mean, m.n) == (3.0, 2) and m.std_dev == pytest.approx(np.sqrt(2.0))
+
+
+def test_ks_identical_samples_as_reference(ref):
+    from paper_2508_16639_b200 import stats as S
+
+    assert S.ks_two_sample_pvalue([1.0, 2.0, 3.0], [1.0, 2.0, 3.0]) == ref.ks([1.0, 2.0, 3.0], [1.0, 2.0, 3.0])
