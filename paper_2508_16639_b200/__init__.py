@@ -5,13 +5,13 @@ this package is the host-side mirror of the reference's C++ API (escg::simulate 
 """
 from .engine import (PAPER_SPECIES, ActionRates, DensityTrace, DeviceEngine, DominanceModel, EngineMode, Lattice,
                      Neighbourhood, RunHooks, RunState, RunStatus, SimParams, SimulationResult, action_rates,
-                     align_num_randoms, is_save_mcs, make_circulant, make_park8, make_rpsls, make_rpsls_ablated,
+                     align_num_randoms, densities, is_save_mcs, make_circulant, make_park8, make_rpsls, make_rpsls_ablated,
                      simulate, stasis, thresholds)
 from .errors import ConfigError, EngineError, FormatError, IoError
 
 __all__ = [
     "PAPER_SPECIES", "ActionRates", "DensityTrace", "DeviceEngine", "DominanceModel", "EngineMode", "Lattice",
     "Neighbourhood", "RunHooks", "RunState", "RunStatus", "SimParams", "SimulationResult", "action_rates",
-    "align_num_randoms", "is_save_mcs", "make_circulant", "make_park8", "make_rpsls", "make_rpsls_ablated",
+    "align_num_randoms", "densities", "is_save_mcs", "make_circulant", "make_park8", "make_rpsls", "make_rpsls_ablated",
     "simulate", "stasis", "thresholds", "ConfigError", "EngineError", "FormatError", "IoError",
 ]

@@ -254,6 +254,16 @@ class DensityTrace:
         self.counts.append(row)
 
 
+def densities(lattice: Lattice, species: int) -> np.ndarray:
+    """engine.cpp:70-94 — counts[v] for v in [0, S] of a host lattice; EngineError on a value outside
+    [0, S].  (Device lattices are counted in the kernels: DeviceEngine.counts.)"""
+    cells = np.asarray(lattice.cells)
+    bad = (cells < 0) | (cells > species)
+    if bad.any():
+        raise EngineError("corrupt lattice value %d" % int(cells[np.argmax(bad)]))
+    return np.bincount(cells.astype(np.int64), minlength=species + 1).astype(np.uint64)
+
+
 def stasis(trace: DensityTrace) -> bool:
     """engine.hpp:40-43"""
     if not trace.counts:

@@ -73,6 +73,11 @@ def _parse_double(text, what):
         raise FormatError("invalid number '%s' for %s" % (text, what))
 
 
+def parse_double(text: str, what: str) -> float:
+    """persistence.hpp parse_double: FormatError naming `what` on anything but a finite number."""
+    return _parse_double(text, what)
+
+
 def _parse_bool(text, what):
     if text in ("true", "1"):
         return True

@@ -154,3 +154,13 @@ def test_build_targets_sm100a():
     lib = os.path.join(ROOT, "paper_2508_16639_b200", "libescg_b200.so")
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib], capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_host_densities_mirror_reference_semantics(escg):
+    """engine.cpp:70-94: counts per value in [0, S]; a value outside raises EngineError."""
+    lat = escg.Lattice(3, 2, np.array([0, 1, 2, 2, 3, 0], np.int32))
+    assert escg.densities(lat, 3).tolist() == [2, 1, 2, 1]
+    with pytest.raises(escg.EngineError, match="corrupt lattice value 4"):
+        escg.densities(escg.Lattice(2, 1, np.array([1, 4], np.int32)), 3)
+    with pytest.raises(escg.EngineError, match="corrupt lattice value -1"):
+        escg.densities(escg.Lattice(2, 1, np.array([-1, 0], np.int32)), 3)
