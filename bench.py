@@ -175,14 +175,19 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic():
-    """DRAM bytes per launch of the dominant kernel from the committed ncu summary (profiles/)."""
+def ncu_summary():
+    """Per-launch figures of the dominant kernel from the committed ncu summary (profiles/)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        d = json.load(open(path))
-        return d.get("dram_bytes_per_launch"), d.get("mcs_per_launch")
+        return json.load(open(path))
     except Exception:
-        return None, None
+        return {}
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel (ncu dram__bytes_read + write)."""
+    d = ncu_summary()
+    return d.get("dram_bytes_per_launch"), d.get("mcs_per_launch")
 
 
 def run_ours(args):
@@ -304,6 +309,18 @@ def run_ours(args):
                         "d2h_bytes_per_step": 4 * N + n_records * (8 + 4 * 8) + 8,
                         "path": "escg_simulate C ABI (simulate() mirror), pinned host int32 lattice in/out"},
                 "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
+        # the binding limit: warp-instruction issue (148 SMs x 4 schedulers x 1 instr/clk); warp
+        # instructions per attempt from the committed ncu capture of this kernel and launch shape
+        summ = ncu_summary()
+        clocks = line["clocks"]
+        if summ.get("warp_inst_per_launch") and summ.get("mcs_per_launch") and clocks.get("sm_mhz"):
+            wipa = summ["warp_inst_per_launch"] / (summ["mcs_per_launch"] * N)
+            peak_issue = 148 * 4 * clocks["sm_mhz"] * 1e6
+            line["issue"] = {"bound": "warp-instruction issue", "warp_inst_per_attempt": wipa,
+                             "achieved": per_gpu * wipa, "peak": peak_issue, "unit": "warp instr/s",
+                             "frac": per_gpu * wipa / peak_issue,
+                             "source": "ncu smsp__inst_executed.sum of one %d-MCS launch (profiles/ncu_summary.json)"
+                                       % summ["mcs_per_launch"]}
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline()

@@ -69,6 +69,7 @@ def main():
     wb = float(big["dram__bytes_write.sum"]) * scale.get(units.get("dram__bytes_write.sum", "byte"), 1)
     summ["dram_bytes_per_launch"] = rb + wb
     summ["mcs_per_launch"] = int(sys.argv[4]) if len(sys.argv) > 4 else None
+    summ["warp_inst_per_launch"] = float(big["smsp__inst_executed.sum"])
     json.dump(summ, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
     det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
     open(os.path.join(prof, "%s_block_kernel_ncu_details.txt" % tag), "w").write(det)
