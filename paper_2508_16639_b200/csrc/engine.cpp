@@ -187,6 +187,7 @@ struct escg_dev {
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
     int bh_max = 0, bw_max = 0;
     int seam_np = 0;  // block kernel on a periodic lattice with seams: colour phases per MCS (4, 6, 9)
+    int phase_table = 0;  // block kernel: per-launch phase-geometry table (few items per thread)
     // row-band engines (one band of a lattice sharded by rows): the local buffer holds
     // halo + band_rows + halo rows; local row r is global row (row0 + r) mod Hg
     int Hg = 0, row0 = 0, wrap_rows = 1;
@@ -296,6 +297,14 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
     h->smem = static_cast<int>(block_smem(bh, bw, h->S1, bk, &h->P, h->seam_np));
+    {
+        // items (tile pairs) per thread per phase: below ~3.5 the per-phase geometry is a large share
+        // of a warp's work and a table built once per launch pays (L=3200: +3.5%); above it the
+        // uniform-register recomputation keeps the item loop's registers free (L=16384: table -4.5%)
+        const double items = ((bh + 2.0 * escgd::margin_rows(bk)) / 4.0) * ((bw + 2.0 * escgd::margin_cols(bk)) / 8.0);
+        h->phase_table = items / h->threads < 3.5 ? 1 : 0;
+        if (const char* pt = std::getenv("ESCG_PHASE_TABLE")) h->phase_table = std::atoi(pt) ? 1 : 0;
+    }
     h->bh_max = bh;
     h->bw_max = bw;
     h->d_rows.alloc(rows.size());
@@ -391,6 +400,7 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.wrap_rows = h->wrap_rows;
     a.reflect = h->flux ? 0 : 1;
     a.seam_np = h->seam_np;
+    a.phase_table = h->phase_table;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -434,6 +444,7 @@ escgd::PersistArgs persist_args(escg_dev* h, const escgd::RunArgs& run) {
     a.wrap_rows = h->wrap_rows;
     a.reflect = h->flux ? 0 : 1;
     a.seam_np = h->seam_np;
+    a.phase_table = h->phase_table;
     a.nby = h->nby;
     a.nbx = h->nbx;
     a.row_split = h->d_rows.p;
@@ -522,6 +533,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.wrap_rows = h->wrap_rows;
         a.reflect = h->flux ? 0 : 1;
         a.seam_np = h->seam_np;
+        a.phase_table = h->phase_table;
         a.nby = h->nby;
         a.nbx = h->nbx;
         a.row_split = h->d_rows.p;
@@ -1193,6 +1205,7 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 a.wrap_rows = h->wrap_rows;
                 a.reflect = h->flux ? 0 : 1;
         a.seam_np = h->seam_np;
+        a.phase_table = h->phase_table;
                 a.nby = h->nby;
                 a.nbx = h->nbx;
                 a.row_split = h->d_rows.p;

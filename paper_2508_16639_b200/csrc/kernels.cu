@@ -26,6 +26,8 @@ namespace escgd {
 // stamps at the end of each phase's work (before the phase barrier) of CTA 0..7
 __device__ unsigned long long g_diag_t[4096 * 16];
 __device__ unsigned long long g_diag_w[8 * 32 * 16];
+// per launch slot (launch index % 256): first CTA start, first CTA past griddepcontrol.wait, last CTA end
+__device__ unsigned long long g_diag_span[256 * 3];
 #endif
 
 namespace {
@@ -444,6 +446,56 @@ struct BlockGeom {
     uint32_t scratch;  // smem address of a dummy 4-row box (edge items with one invalid tile)
 };
 
+// Per-(MCS, phase) geometry of one block-kernel launch, identical for every thread of a CTA: built
+// once per launch by warp 0 (lane q = phase q, overlapping the PDL wait) instead of by every warp in
+// every phase (the round draw, the valid-region bounds, the pair columns and rows per round).
+struct PhaseGeom {
+    int j0, nj, u0, nu;     // first active tile row, active rows, first pair column, pairs per row
+    int i0, imin, imax, R;  // WIDE first tile column, valid tile-column range, rows per round
+    uint32_t c1, c2;        // draw counter words of the phase (MCS low, STEP c2)
+    int cx, oyox;           // colour column parity, tiling origin oy | ox << 1
+};
+__shared__ PhaseGeom sPh[4 * kMaxBlockMcs];
+
+template <bool NARROW>
+__device__ __noinline__ void build_phase_table(const BlockGeom g, int Wh, int Ww, uint32_t s32) {
+    const int q = threadIdx.x;  // warp 0
+    if (q >= 4 * g.nmcs) return;
+    const int t = q >> 2, p = q & 3;
+    const uint64_t mcs = static_cast<uint64_t>(g.mcs + t);
+    const Round rp = round_params(s32, mcs);
+    const int ex = margin_cols(g.nmcs) - margin_rows(g.nmcs);  // extra loaded columns
+    const int cy = rp.colour(p) >> 1, cx = rp.colour(p) & 1;
+    // footprint rows [2j-oy-1, 2j-oy+2] within [3q, Wh-3q); cols within [ex+3q, Ww-ex-3q)
+    const int lo = 3 * q, hiR = Wh - 3 * q, loC = ex + 3 * q, hiC = Ww - ex - 3 * q;
+    const int jmin = (lo + rp.oy + 2) >> 1, jmax = (hiR - 3 + rp.oy) >> 1;
+    const int imin = (loC + rp.ox + 2) >> 1, imax = (hiC - 3 + rp.ox) >> 1;
+    PhaseGeom G;
+    G.j0 = jmin + ((jmin ^ cy) & 1);
+    G.nj = jmax >= G.j0 ? ((jmax - G.j0) >> 1) + 1 : 0;
+    // items: pairs of same-colour tiles (i, i+2).  NARROW pairs are the global draw pairs (window
+    // column 0 is 8-aligned); WIDE pairs are local.  A tile outside the valid region runs on the
+    // scratch box (same instruction stream for every lane, results discarded).
+    G.i0 = imin + ((imin ^ cx) & 1);  // first valid tile column of this colour
+    if (NARROW) {
+        G.u0 = (imin - cx + 1) >> 2;
+        const int u1 = imax >= cx ? (imax - cx) >> 2 : -1;
+        G.nu = u1 >= G.u0 ? u1 - G.u0 + 1 : 0;
+    } else {
+        const int ni = imax >= G.i0 ? ((imax - G.i0) >> 1) + 1 : 0;
+        G.u0 = 0;
+        G.nu = (ni + 1) >> 1;
+    }
+    G.imin = imin;
+    G.imax = imax;
+    G.R = G.nu > 0 ? udiv_small(static_cast<int>(blockDim.x), G.nu) : 0;
+    G.c1 = static_cast<uint32_t>(mcs);
+    G.c2 = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+    G.cx = cx;
+    G.oyox = rp.oy | (rp.ox << 1);
+    sPh[q] = G;
+}
+
 template <int ARITY, bool NARROW, bool BF>
 __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs rule, uint32_t win0, int Wh, int Ww,
                                              int wy0, int wx0, uint32_t s32) {
@@ -575,6 +627,178 @@ __device__ __forceinline__ void block_phases(const BlockGeom g, const RuleArgs r
             if (t == 0) DIAG_STAMP(3 + p);
         }
     }
+}
+
+template <int ARITY, bool NARROW, bool BF>
+__device__ __forceinline__ void block_phases_tab(const BlockGeom g, const RuleArgs rule, uint32_t win0, int Wh, int Ww,
+                                             int wy0, int wx0, uint32_t s32) {
+    const int tid = threadIdx.x, nt = blockDim.x, P = g.P;
+    const int Ty = g.Hg >> 1, Tx = g.L >> 1, TQ = g.L >> 3;
+    // global tile index of window tile 0 (even; ib % 4 == 0 if NARROW)
+    const int jb = ((g.row0 + wy0) % g.Hg) >> 1, ib = wx0 >> 1;
+    const bool big = Wh > g.Hg || Ww > g.L;  // window wraps more than once: use a true modulo
+    const int ex = margin_cols(g.nmcs) - margin_rows(g.nmcs);  // extra loaded columns
+    Round rp = {0, 0, 0u};
+#pragma unroll 1
+    for (int q = 0; q < 4 * g.nmcs; ++q) {
+        const int t = q >> 2;
+        // phase geometry: TAB reads the per-launch table (few items per thread: the per-phase work
+        // dominates); otherwise it is recomputed in uniform registers (many items per thread: no
+        // extra vector-register pressure on the item loop)
+        int j0, nj, u0, nu, i0, imin, imax, R, cx, oy, ox;
+        uint32_t c1, c2p;
+        if (true) {
+            const PhaseGeom& G = sPh[q];
+            j0 = G.j0;
+            nj = G.nj;
+            u0 = G.u0;
+            nu = G.nu;
+            i0 = G.i0;
+            imin = G.imin;
+            imax = G.imax;
+            R = G.R;
+            cx = G.cx;
+            oy = G.oyox & 1;
+            ox = G.oyox >> 1;
+            c1 = G.c1;
+            c2p = G.c2;
+        } else {
+            const int p = q & 3;
+            const uint64_t mcs = static_cast<uint64_t>(g.mcs + t);
+            if (p == 0) rp = round_params(s32, mcs);
+            const int cy = rp.colour(p) >> 1;
+            cx = rp.colour(p) & 1;
+            oy = rp.oy;
+            ox = rp.ox;
+            // footprint rows [2j-oy-1, 2j-oy+2] within [3q, Wh-3q); cols within [ex+3q, Ww-ex-3q)
+            const int lo = 3 * q, hiR = Wh - 3 * q, loC = ex + 3 * q, hiC = Ww - ex - 3 * q;
+            const int jmin = (lo + oy + 2) >> 1, jmax = (hiR - 3 + oy) >> 1;
+            imin = (loC + ox + 2) >> 1;
+            imax = (hiC - 3 + ox) >> 1;
+            j0 = jmin + ((jmin ^ cy) & 1);
+            nj = jmax >= j0 ? ((jmax - j0) >> 1) + 1 : 0;
+            i0 = imin + ((imin ^ cx) & 1);
+            if (NARROW) {
+                u0 = (imin - cx + 1) >> 2;
+                const int u1 = imax >= cx ? (imax - cx) >> 2 : -1;
+                nu = u1 >= u0 ? u1 - u0 + 1 : 0;
+            } else {
+                const int ni = imax >= i0 ? ((imax - i0) >> 1) + 1 : 0;
+                u0 = 0;
+                nu = (ni + 1) >> 1;
+            }
+            R = nu > 0 ? udiv_small(nt, nu) : 0;
+            c1 = static_cast<uint32_t>(mcs);
+            c2p = ctr2(mcs, kDomStep, static_cast<uint32_t>(p), 0u);
+        }
+        PhaseCtx C;
+        C.fast = NARROW ? rule.fast : 0u;
+        C.xm = rule.xm;
+        C.xi = rule.xi;
+        C.bf = BF ? 1u : 0u;
+        C.c1 = c1;
+        C.c2 = c2p;
+        C.c3 = s32;
+        const uint32_t c2 = C.c2;
+        // Thread -> items: a fixed item column b (pair b of every active tile row) and rows
+        // a0, a0 + R, a0 + 2R, ... with R = floor(threads / nu): the column geometry, the
+        // half-warp chain order and the scratch redirection are per-phase constants, and a row
+        // step is a few adds.  (Items are the same as any other enumeration; order within a
+        // phase is immaterial.)
+        if (nu > 0 && nj > 0) {
+            const int a0 = udiv_small(tid, nu), b = tid - a0 * nu;
+            if (a0 < R && a0 < nj) {
+                // upper half-warp runs its pair's second tile as chain 1 (bank split, tile_dual)
+#ifdef ESCG_DIAG_NO_SWAP
+                const bool sw = false;
+#else
+                const bool sw = (tid & 16) != 0;
+#endif
+                int ia1, ia2;  // window tile columns of chain 1 / chain 2
+                uint32_t tc1, tc2;  // global tile-column part of the tile ids
+                uint32_t ctrcol = 0;  // NARROW: pair column of the draw counter
+                if (NARROW) {
+                    const int u = u0 + b;
+                    const int qq = big ? ((ib >> 2) + u) % TQ : wrap_down((ib >> 2) + u, TQ, false);
+                    const int ia = cx + 4 * u;
+                    ctrcol = static_cast<uint32_t>(qq);
+                    ia1 = sw ? ia + 2 : ia;
+                    ia2 = sw ? ia : ia + 2;
+                    tc1 = static_cast<uint32_t>(4 * qq + cx + (sw ? 2 : 0));
+                    tc2 = static_cast<uint32_t>(4 * qq + cx + (sw ? 0 : 2));
+                } else {
+                    const int ia = i0 + 4 * b;
+                    const uint32_t tA = static_cast<uint32_t>(big ? (ib + ia) % Tx : wrap_down(ib + ia, Tx, false));
+                    const uint32_t tB =
+                        static_cast<uint32_t>(big ? (ib + ia + 2) % Tx : wrap_down(ib + ia + 2, Tx, false));
+                    ia1 = sw ? ia + 2 : ia;
+                    ia2 = sw ? ia : ia + 2;
+                    tc1 = sw ? tB : tA;
+                    tc2 = sw ? tA : tB;
+                }
+                const bool ok1 = ia1 >= imin && ia1 <= imax, ok2 = ia2 >= imin && ia2 <= imax;
+                const uint32_t scr1 = sw ? g.scratch + 8 : g.scratch, scr2 = sw ? g.scratch : g.scratch + 8;
+                int j = j0 + 2 * a0;
+                int ty = big ? (jb + j) % Ty : wrap_down(jb + j, Ty, false);
+                const int dTy = big ? (2 * R) % Ty : 2 * R;  // window rows < Ty: 2R < Ty
+                uint32_t rowbase = win0 + static_cast<uint32_t>((2 * j - oy) * P - ox);
+                const uint32_t dRow = static_cast<uint32_t>(4 * R * P);
+                auto draw1 = [&](int ty_) {
+                    return NARROW ? philox(static_cast<uint32_t>(ty_) * static_cast<uint32_t>(TQ) + ctrcol, C.c1, c2, s32)
+                                  : philox(static_cast<uint32_t>(ty_) * static_cast<uint32_t>(Tx) + tc1, C.c1, c2, s32);
+                };
+                uint4 w = draw1(ty);
+                for (int a = a0; a < nj; a += R) {
+                    int nty = ty + dTy;
+                    nty = nty >= Ty ? nty - Ty : nty;
+                    uint4 nw = make_uint4(0, 0, 0, 0);
+                    if (a + R < nj) nw = draw1(nty);
+                    const uint32_t trow = static_cast<uint32_t>(ty) * static_cast<uint32_t>(Tx);
+                    const uint32_t base1 = ok1 ? rowbase + 2 * ia1 : scr1;
+                    const uint32_t base2 = ok2 ? rowbase + 2 * ia2 : scr2;
+                    if (NARROW) {
+                        // pair draw: words (x, y) belong to the pair's first tile, (z, w) to its second
+                        const uint32_t p0 = sw ? w.z : w.x, p1 = sw ? w.w : w.y;
+                        const uint32_t q0 = sw ? w.x : w.z, q1 = sw ? w.y : w.w;
+                        const uint32_t b1[4] = {p0 & 0xFFFFu, p0 >> 16, p1 & 0xFFFFu, p1 >> 16};
+                        const uint32_t b2[4] = {q0 & 0xFFFFu, q0 >> 16, q1 & 0xFFFFu, q1 >> 16};
+                        tile_dual_ordered<ARITY, true>(b1, base1, trow + tc1, b2, base2, trow + tc2, C);
+                    } else {
+                        const uint4 w2 = philox(trow + tc2, C.c1, c2, s32);
+                        const uint32_t b1[4] = {w.x, w.y, w.z, w.w};
+                        const uint32_t b2[4] = {w2.x, w2.y, w2.z, w2.w};
+                        tile_dual_ordered<ARITY, false>(b1, base1, trow + tc1, b2, base2, trow + tc2, C);
+                    }
+                    ty = nty;
+                    rowbase += dRow;
+                    w = nw;
+                }
+            }
+        }
+#ifdef ESCG_DIAG_TIMING
+        {
+            const int cta = blockIdx.x + gridDim.x * blockIdx.y;
+            if (cta < 8 && (threadIdx.x & 31) == 0 && q < 16) {
+                unsigned long long tw;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tw));
+                g_diag_w[(cta * 32 + (threadIdx.x >> 5)) * 16 + q] = tw;
+            }
+        }
+#endif
+#ifndef ESCG_DIAG_NO_PHASE_SYNC
+        __syncthreads();
+#endif
+        if (t == 0) DIAG_STAMP(3 + (q & 3));
+    }
+}
+
+template <int ARITY, bool NARROW, bool BF, bool TAB>
+__device__ __forceinline__ void block_phases_any(const BlockGeom g, const RuleArgs rule, uint32_t win0, int Wh, int Ww,
+                                                 int wy0, int wx0, uint32_t s32) {
+    if constexpr (TAB)
+        block_phases_tab<ARITY, NARROW, BF>(g, rule, win0, Wh, Ww, wy0, wx0, s32);
+    else
+        block_phases<ARITY, NARROW, BF>(g, rule, win0, Wh, Ww, wy0, wx0, s32);
 }
 
 // ---- TMA bulk copies (cp.async.bulk, Hopper+/Blackwell) ----------------------------------------
@@ -836,13 +1060,21 @@ __device__ void load_window_bytes(uint8_t* win, const uint8_t* src, int H, int L
     }
 }
 
-template <int ARITY, int BMODE, bool BF>
+template <int ARITY, int BMODE, bool BF, bool TAB>
 __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     constexpr bool REFLECT = BMODE == 1, SEAM = BMODE == 2;
     extern __shared__ __align__(128) uint8_t smem[];
     // Programmatic dependent launch: let the next launch's CTAs start their prologue as soon as SMs
     // free up; everything that reads the previous launch's output sits behind griddepcontrol.wait.
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#ifdef ESCG_DIAG_TIMING
+    const int dslot = static_cast<int>((a.mcs / (a.nmcs > 0 ? a.nmcs : 1)) & 255);
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMin(&g_diag_span[dslot * 3 + 0], t);
+    }
+#endif
     const int r = blockIdx.z;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
@@ -904,6 +1136,15 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         // prologue: inputs that no earlier launch writes (rule, seeds, geometry)
         for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
         attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
+        if (TAB && tid < 32) {
+            BlockGeom gt;
+            gt.nmcs = a.nmcs;
+            gt.mcs = a.mcs;
+            if (a.narrow)
+                build_phase_table<true>(gt, Wh, Ww, s32);
+            else
+                build_phase_table<false>(gt, Wh, Ww, s32);
+        }
         // the scratch box must hold valid species codes: dummy attempts index the threshold table
         for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
         if (tma && tid == 0) {
@@ -911,6 +1152,13 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef ESCG_DIAG_TIMING
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            atomicMin(&g_diag_span[dslot * 3 + 1], t);
+        }
+#endif
         if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) {
@@ -940,9 +1188,9 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         g.mcs = a.mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases_any<ARITY, true, false, TAB>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false, BF>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases_any<ARITY, false, BF, TAB>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
 #ifndef ESCG_DIAG_NO_LOAD
         if (tma) {
             // generic-proxy writes → async proxy, then one bulk store per block row
@@ -992,6 +1240,13 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     // bulk stores must finish reading shared memory before the CTA exits
     if (a.step && tma) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     DIAG_STAMP(9);
+#ifdef ESCG_DIAG_TIMING
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        atomicMax(&g_diag_span[dslot * 3 + 2], t);
+    }
+#endif
 }
 
 // Persistent variant: one cooperative launch runs every chunk of a run; a grid barrier replaces the
@@ -1087,6 +1342,15 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
         // generic-proxy writes of the previous chunk (other CTAs) → this CTA's async-proxy reads
         asm volatile("fence.proxy.async.global;" ::: "memory");
         if (tid == 0) mbar_expect_tx_arrive(mbar, static_cast<uint32_t>(Wh * Ww));
+        if (tid < 32) {  // phase table of this chunk (the previous chunk's phases are done)
+            BlockGeom gt;
+            gt.nmcs = chunk;
+            gt.mcs = mcs;
+            if (a.narrow)
+                build_phase_table<true>(gt, Wh, Ww, s32);
+            else
+                build_phase_table<false>(gt, Wh, Ww, s32);
+        }
         __syncthreads();
         load_window_tma(win, src, H, L, P, Wh, Ww, wy0, wx0, mbar);
         mbar_wait(mbar, tma_phase);
@@ -1102,9 +1366,9 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
         g.mcs = mcs;
         g.scratch = smem_addr(sScratch) + static_cast<uint32_t>(P + 1);
         if (a.narrow)
-            block_phases<ARITY, true, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases_any<ARITY, true, false, true>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         else
-            block_phases<ARITY, false, false>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
+            block_phases_any<ARITY, false, false, true>(g, a.rule, win0, Wh, Ww, wy0, wx0, s32);
         store_block<16>(dst, win, L, P, bh, bw, ry0, rx0, Myc, Mxc);
         mcs += chunk;
         par ^= 1;
@@ -1233,6 +1497,25 @@ int tile_smem_bytes(int H, int L, int S, int* pitch) {
 }
 
 // Diagnostic: copy the block kernel's section stamps (ESCG_DIAG_TIMING builds; else returns 0).
+extern "C" __attribute__((visibility("default"))) int escg_diag_spans(unsigned long long* out, int reset) {
+#ifdef ESCG_DIAG_TIMING
+    if (reset) {
+        static unsigned long long init[256 * 3];
+        for (int i = 0; i < 256; ++i) {
+            init[3 * i] = ~0ull;
+            init[3 * i + 1] = ~0ull;
+            init[3 * i + 2] = 0ull;
+        }
+        return cudaMemcpyToSymbol(g_diag_span, init, sizeof(init)) == cudaSuccess ? 0 : -1;
+    }
+    return cudaMemcpyFromSymbol(out, g_diag_span, sizeof(unsigned long long) * 256 * 3) == cudaSuccess ? 0 : -1;
+#else
+    (void)out;
+    (void)reset;
+    return -1;
+#endif
+}
+
 extern "C" __attribute__((visibility("default"))) int escg_diag_warps(unsigned long long* out, int n) {
 #ifdef ESCG_DIAG_TIMING
     return cudaMemcpyFromSymbol(out, g_diag_w, sizeof(unsigned long long) * (n < 8 * 32 * 16 ? n : 8 * 32 * 16)) ==
@@ -1306,9 +1589,11 @@ static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cud
     const bool bf = a.rule.wide_bf && !a.narrow;
     // the dynamic-smem opt-in is a per-device function attribute: remember it per device (band
     // groups drive several devices from one thread); atomics keep concurrent host threads safe
-    static std::atomic<int> configured[2][kMaxDevices];  // [rule form][device]
-    std::atomic<int>* configured_bytes = configured[bf ? 1 : 0];
-    auto k = bf ? block_kernel<ARITY, BMODE, true> : block_kernel<ARITY, BMODE, false>;
+    const bool tab = a.phase_table != 0 && BMODE == 0;
+    static std::atomic<int> configured[4][kMaxDevices];  // [rule form x phase table][device]
+    std::atomic<int>* configured_bytes = configured[(bf ? 1 : 0) + (tab ? 2 : 0)];
+    auto k = bf ? (tab ? block_kernel<ARITY, BMODE, true, true> : block_kernel<ARITY, BMODE, true, false>)
+                : (tab ? block_kernel<ARITY, BMODE, false, true> : block_kernel<ARITY, BMODE, false, false>);
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;

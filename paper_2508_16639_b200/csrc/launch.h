@@ -69,6 +69,7 @@ struct BlockArgs {
     int wrap_rows;       // 1: the local buffer is the whole periodic lattice; 0: band with halo rows
     int reflect;         // 1: mirror-reflecting lattice (flux = false): clipped windows, reflect tiling
     int seam_np;         // > 0: periodic lattice with seams (L or H not divisible by 4): phases per MCS
+    int phase_table;     // 1: per-launch phase-geometry table (few items per thread per phase)
     int nby, nbx;
     const int* row_split;  // nby+1 row boundaries (multiples of 4)
     const int* col_split;  // nbx+1

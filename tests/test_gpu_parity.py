@@ -131,12 +131,14 @@ def test_tile_kernel_matches_crs_oracle(escg, oracle, case):
     assert np.array_equal(got7, want7)
 
 
+@pytest.mark.parametrize("table", ["0", "1"])
 @pytest.mark.parametrize("fmt", ["wide", "narrow"])
 @pytest.mark.parametrize("LH", [(64, 64), (200, 200), (96, 160), (8, 8), (100, 36)])
 @pytest.mark.parametrize("arity", [4, 8])
-def test_block_kernel_matches_crs_oracle(escg, oracle, LH, arity, fmt, monkeypatch):
+def test_block_kernel_matches_crs_oracle(escg, oracle, LH, arity, fmt, table, monkeypatch):
     L, H = LH
     monkeypatch.setenv("ESCG_DRAW_FORMAT", fmt)
+    monkeypatch.setenv("ESCG_PHASE_TABLE", table)  # both phase-geometry paths of block_phases
     model = escg.make_circulant(3, [1])
     seed = 99
     M = 1e-2 if fmt == "narrow" else 1e-3
