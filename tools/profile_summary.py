@@ -40,7 +40,9 @@ def main():
     tot = sum(sum(v) for v in agg.values())
     lines = ["# %s launch list (ncu --metrics gpu__time_duration.sum --clock-control none)" % tag, "",
              "Command: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline` (first 700 launches).",
-             "Per-launch times are cold-cache and serialised (compare shares, not absolutes).", "",
+             "Per-launch times are cold-cache and serialised (compare shares, not absolutes).",
+             "Full capture (`*_block_kernel_ncu_details.txt`, `ncu_summary.json`): one steady-state 2-MCS launch of "
+             "`python tools/one_block.py 3200 200` (ncu --set full -s 50 -c 1), the bench's block kernel shape.", "",
              "| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
     for k, v in agg.items():
         lines.append("| %s | %d | %.2f | %.1f | %.1f%% |" % (k, len(v), sum(v) / len(v), sum(v), 100 * sum(v) / tot))
