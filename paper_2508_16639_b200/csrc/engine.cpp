@@ -755,8 +755,30 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         const bool periodic4 = h->flux && (h->H % 4 == 0) && (h->L % 4 == 0);
         if (h->flux && (h->H < 4 || h->L < 4))
             config_error("device engine: periodic lattices need L, H >= 4 (2x2 tiles, footprints may not wrap)");
+        // tile-kernel CTA size: ~2.5 items (tile pairs) per thread and phase, so small lattices get
+        // small CTAs and more replicas share an SM (measured: L=64 → 64 threads, L=100 → 128, L >= 200 → 512)
+        int tile_threads;
+        {
+            const int64_t items = ((h->H + 3) / 4) * (int64_t)((h->L + 7) / 8);
+            int64_t tt = (items * 2 / 5) / 32 * 32;
+            tt = tt > 448 ? 512 : std::max<int64_t>(64, tt);
+            tile_threads = static_cast<int>(tt);
+            if (const char* tv = std::getenv("ESCG_TILE_THREADS"))
+                tile_threads = std::max(32, std::min(512, (std::atoi(tv) + 31) / 32 * 32));
+        }
         int choice = kernel;
-        if (choice == ESCG_KERNEL_AUTO) choice = tbytes <= smem_cap ? ESCG_KERNEL_TILE : ESCG_KERNEL_BLOCK;
+        if (choice == ESCG_KERNEL_AUTO) {
+            // one CTA per replica (tile) wins only when the replicas fill the device: at least one
+            // per SM and a quarter of the tile kernel's concurrent CTAs; fewer lattices run faster
+            // spread over all SMs by the block kernel (measured on B200: one L=200 lattice 5.2e9 vs
+            // 1.5e9 attempts/s; 148 replicas of L=200 2.2e11 tile vs 1.7e11 block)
+            choice = ESCG_KERNEL_BLOCK;
+            if (tbytes <= smem_cap && !bs) {
+                const int slots = escgd::tile_capacity(h->arity, h->flux, h->H, h->L, tile_threads, tbytes, device);
+                if (n_replicas >= prop.multiProcessorCount && 4 * static_cast<int64_t>(n_replicas) >= slots)
+                    choice = ESCG_KERNEL_TILE;
+            }
+        }
         if (choice == ESCG_KERNEL_TILE && tbytes > smem_cap)
             config_error("lattice too large for the shared-memory tile kernel");
         if (choice == ESCG_KERNEL_BLOCK && h->flux && !periodic4) {
@@ -786,15 +808,7 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
         if (choice == ESCG_KERNEL_TILE) {
             h->P = tpitch;
             h->smem = tbytes;
-            // ~2.5 items (tile pairs) per thread and phase: small lattices get small CTAs, so more
-            // replicas share an SM and fewer lanes idle (measured: L=64 → 64 threads, L=100 → 128,
-            // L >= 200 → 512)
-            const int64_t items = ((h->H + 3) / 4) * (int64_t)((h->L + 7) / 8);
-            int64_t tt = (items * 2 / 5) / 32 * 32;
-            tt = tt > 448 ? 512 : std::max<int64_t>(64, tt);
-            h->threads = static_cast<int>(tt);
-            if (const char* tv = std::getenv("ESCG_TILE_THREADS"))
-                h->threads = std::max(32, std::min(512, (std::atoi(tv) + 31) / 32 * 32));
+            h->threads = tile_threads;
         } else {
             h->lat[1].alloc(static_cast<size_t>(h->N) * n_replicas);
             // lattices far beyond one CTA per SM stream through many waves: two 512-thread CTAs per

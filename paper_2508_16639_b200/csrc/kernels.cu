@@ -1623,6 +1623,25 @@ static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cud
     return cudaLaunchKernelEx(&cfg, k, a);
 }
 
+// Concurrent tile-kernel CTAs (one per replica) the device holds at this CTA shape.
+int tile_capacity(int arity, int flux, int H, int L, int threads, int smem_bytes, int device) {
+    const int mode = !flux ? kModeReflect : ((H % 4 == 0 && L % 4 == 0) ? kModePeriodic : kModeSeam);
+    const void* f = nullptr;
+    if (arity == 8)
+        f = mode == kModeReflect ? reinterpret_cast<const void*>(tile_kernel<8, kModeReflect, false>)
+            : mode == kModeSeam  ? reinterpret_cast<const void*>(tile_kernel<8, kModeSeam, false>)
+                                 : reinterpret_cast<const void*>(tile_kernel<8, kModePeriodic, false>);
+    else
+        f = mode == kModeReflect ? reinterpret_cast<const void*>(tile_kernel<4, kModeReflect, false>)
+            : mode == kModeSeam  ? reinterpret_cast<const void*>(tile_kernel<4, kModeSeam, false>)
+                                 : reinterpret_cast<const void*>(tile_kernel<4, kModePeriodic, false>);
+    int per_sm = 0, sms = 0;
+    if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem_bytes) != cudaSuccess) return 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return per_sm * sms;
+}
+
 int block_persistent_capacity(int arity, int threads, int smem_bytes, int device) {
     int per_sm = 0, sms = 0;
     auto k4 = block_kernel_persistent<4>;

@@ -122,6 +122,7 @@ cudaError_t launch_tile(const TileArgs& a, int nrep, int threads, cudaStream_t s
 cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t s);
 cudaError_t launch_block_persistent(const PersistArgs& a, int nrep, int threads, cudaStream_t s);
 int block_persistent_capacity(int arity, int threads, int smem_bytes, int device);
+int tile_capacity(int arity, int flux, int H, int L, int threads, int smem_bytes, int device);
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
 cudaError_t launch_u8_to_i32(const uint8_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_i32_to_u8(const int32_t* src, uint8_t* dst, int64_t n, int S, int* bad, cudaStream_t s);

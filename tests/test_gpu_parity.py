@@ -371,7 +371,7 @@ def test_seam_lattice_ensemble_matches_oracle(escg, oracle):
     L, H, S = 31, 29, 3
     model = escg.make_circulant(3, [1])
     p = params(escg, L, H, S, 1e-3, 0.1, 4, True, seed=5)
-    with escg.DeviceEngine(p, model, n_replicas=6, seeds=range(50, 56)) as eng:
+    with escg.DeviceEngine(p, model, n_replicas=6, seeds=range(50, 56), kernel="tile") as eng:
         assert eng.describe()["kernel"] == "tile"
         eng.init_lattice()
         init = [eng.get_lattice(r) for r in range(6)]
@@ -528,3 +528,16 @@ def test_device_init_lattice_is_uniform(escg, ref):
     n = L * L
     assert abs(c[0] / n - 0.2) < 5 * np.sqrt(0.2 * 0.8 / n)
     assert ref.chi_square_uniform(c[1:]) > 1e-3
+
+
+def test_auto_kernel_choice(escg):
+    """AUTO: replicas that fill the device run one CTA each (tile); a few lattices spread over all
+    SMs (block) — the faster choice on B200 in both regimes (engine.cpp create_impl)."""
+    p = params(escg, 200, 200, 3, 1e-4, 0.1, 4, True)
+    model = escg.make_circulant(3, [1])
+    with escg.DeviceEngine(p, model) as eng:
+        assert eng.describe()["kernel"] == "block"
+    with escg.DeviceEngine(p, model, n_replicas=296, seeds=range(296)) as eng:
+        assert eng.describe()["kernel"] == "tile"
+    with escg.DeviceEngine(params(escg, 3200, 3200, 3, 1e-4, 0.1, 4, True), model) as eng:
+        assert eng.describe()["kernel"] == "block"
