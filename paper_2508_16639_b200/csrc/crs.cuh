@@ -165,8 +165,9 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) {
 //   sSlow    what only the exact (slow) paths and the WIDE rule read: X_mig, X_int, the smem
 //            address of the (S+1)^2 interaction thresholds, S+1.
 struct SlowParams {
-    uint32_t xm, xi, sT;
+    uint32_t xm, xi, sT;  // sT: smem address of the coarse pair table (see fill_pair_thresholds)
     int S1;
+    const uint32_t* gT;   // exact (S+1)^2 thresholds in global memory (rare exact path)
 };
 __shared__ int2 sOffTbl[32];
 __shared__ SlowParams sSlow;
@@ -262,7 +263,7 @@ __device__ __noinline__ uint32_t slow_wide(uint32_t s, uint32_t n, uint32_t word
                                            uint32_t c2, uint32_t c3) {
     constexpr int LB = Bits<ARITY>::LB;
     const uint32_t x = ((word >> LB) << LB) | (refine_word(tile, a, c1, c2, c3) & ((1u << LB) - 1u));
-    return rule_exact_s(s, n, x, sSlow.xm, sSlow.xi, sSlow.sT, sSlow.S1);
+    return rule_exact(s, n, x, sSlow.xm, sSlow.xi, sSlow.gT, sSlow.S1);
 }
 
 // NARROW slow path: x = coarse(16-LB bits) << (16+LB) | low (16+LB) bits of the REFINE word.
@@ -271,7 +272,28 @@ __device__ __noinline__ uint32_t slow_narrow(uint32_t s, uint32_t n, uint32_t ha
                                              uint32_t c1, uint32_t c2, uint32_t c3) {
     constexpr int LB = Bits<ARITY>::LB, SH = 16 + LB;
     const uint32_t x = ((half >> LB) << SH) | (refine_word(tile, a, c1, c2, c3) & ((1u << SH) - 1u));
-    return rule_exact_s(s, n, x, sSlow.xm, sSlow.xi, sSlow.sT, sSlow.S1);
+    return rule_exact(s, n, x, sSlow.xm, sSlow.xi, sSlow.gT, sSlow.S1);
+}
+
+// 64-bit shared load under a predicate (no branch); zeros when the predicate is false.
+__device__ __forceinline__ uint2 lds64_if(bool p, uint32_t a) {
+    uint2 v = make_uint2(0u, 0u);
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t@q ld.shared.v2.u32 {%0, %1}, [%2];\n\t}"
+        : "+r"(v.x), "+r"(v.y)
+        : "r"(a), "r"(static_cast<uint32_t>(p)));
+    return v;
+}
+
+// Coarse pair table of the WIDE rule: entry (s, n) = (T[s][n] & HI, T[n][s] & HI), HI the coarse-bit
+// mask of the attempt word.  A coarse word x (low LB bits zero) decides x_exact < T exactly as
+// x < (T & HI) unless x == T & HI, which is the exact path (exact T from global memory).
+template <int ARITY>
+__device__ __forceinline__ void fill_pair_thresholds(uint2* sTp, const uint32_t* T, int S1) {
+    constexpr uint32_t HI = ~((1u << Bits<ARITY>::LB) - 1u);
+    for (int i = threadIdx.x; i < S1 * S1; i += blockDim.x) {
+        const int s = i / S1, n = i - s * S1;
+        sTp[i] = make_uint2(T[s * S1 + n] & HI, T[n * S1 + s] & HI);
+    }
 }
 
 // 32-bit shared load under a predicate (no branch); `dflt` when the predicate is false.
@@ -308,12 +330,12 @@ __device__ __forceinline__ uint32_t rule_wide(uint32_t s, uint32_t n, uint32_t w
                 else if (s == 0u)
                     ns = n;
             } else if ((s != 0u) & (n != 0u) & (s != n)) {
-                const uint32_t sT = sSlow.sT, S1 = static_cast<uint32_t>(sSlow.S1);
-                const uint32_t t1 = lds32(sT + 4u * (s * S1 + n)), t2 = lds32(sT + 4u * (n * S1 + s));
-                exact = (x == (t1 & HI)) | (x == (t2 & HI));
-                if (x < t1)
+                // coarse pair (T[s][n] & HI, T[n][s] & HI): x < T ⇔ x < (T & HI) unless they are equal
+                const uint2 t = lds64(sSlow.sT + 8u * (s * static_cast<uint32_t>(sSlow.S1) + n));
+                exact = (x == t.x) | (x == t.y);
+                if (x < t.x)
                     nn = 0u;
-                else if (x < t2)
+                else if (x < t.y)
                     ns = 0u;
             }
         }
@@ -322,10 +344,9 @@ __device__ __forceinline__ uint32_t rule_wide(uint32_t s, uint32_t n, uint32_t w
     }
     const bool mig = x < C.xm, rep = x >= C.xi;
     const bool inter = !mig & !rep & (s != 0u) & (n != 0u) & (s != n);
-    const uint32_t sT = sSlow.sT, S1 = static_cast<uint32_t>(sSlow.S1);
-    const uint32_t t1 = lds32_if(inter, sT + 4u * (s * S1 + n), 0u);
-    const uint32_t t2 = lds32_if(inter, sT + 4u * (n * S1 + s), 0u);
-    const bool exact = (x == (C.xm & HI)) | (x == (C.xi & HI)) | (inter & ((x == (t1 & HI)) | (x == (t2 & HI))));
+    const uint2 t = lds64_if(inter, sSlow.sT + 8u * (s * static_cast<uint32_t>(sSlow.S1) + n));
+    const uint32_t t1 = t.x, t2 = t.y;  // coarse (masked) thresholds: see fill_pair_thresholds
+    const bool exact = (x == (C.xm & HI)) | (x == (C.xi & HI)) | (inter & ((x == t1) | (x == t2)));
     const bool k1 = inter & (x < t1);               // u < D[s][n]: the neighbour dies
     const bool k2 = inter & !(x < t1) & (x < t2);   // else u < D[n][s]: the cell dies
     const bool r1 = rep & (n == 0u), r2 = rep & (n != 0u) & (s == 0u);

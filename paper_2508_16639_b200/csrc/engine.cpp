@@ -238,14 +238,14 @@ size_t block_smem(int bh, int bw, int S1, int k, int* pitch, int seam_np = 0) {
         const int Wh = bh + 2 * m, Ww = bw + 2 * m;
         const int P = (Ww + 15) & ~15;
         if (pitch) *pitch = P;
-        return static_cast<size_t>(((Wh * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8 +
+        return static_cast<size_t>(((Wh * P + 15) & ~15) + ((S1 * S1 * 8 + 15) & ~15) + 32 * 8 +
                                    (escgd::kMaxSpecies + 1) * 4 + 4 * P + 64 + 16 +
                                    3 * 16 * ((Wh / 2 + 2) + (Ww / 2 + 2)));
     }
     // pitch ≡ 0 (mod 128 bytes): see tile_dual (bank-conflict-light half-warp split)
     const int P = ((bw + 2 * escgd::margin_cols(k)) + 127) & ~127;
     if (pitch) *pitch = P;
-    return static_cast<size_t>((((bh + 2 * escgd::margin_rows(k)) * P + 15) & ~15) + ((S1 * S1 * 4 + 15) & ~15) +
+    return static_cast<size_t>((((bh + 2 * escgd::margin_rows(k)) * P + 15) & ~15) + ((S1 * S1 * 8 + 15) & ~15) +
                                32 * 8 + (escgd::kMaxSpecies + 1) * 4 + 4 * P + 64);  // + scratch box
 }
 

@@ -175,7 +175,7 @@ __host__ __device__ inline TileSmem tile_layout(int H, int L, int S, int P) {
     const int S1 = S + 1;
     t.lat_bytes = align16((H + 3) * P);
     t.T_off = t.lat_bytes;
-    t.snap_off = t.T_off + align16(S1 * S1 * 4);
+    t.snap_off = t.T_off + align16(S1 * S1 * 8);  // coarse pair table (crs.cuh fill_pair_thresholds)
     t.cnt_off = t.snap_off + align16(3 * (L + 3) + 3 * H);
     t.flag_off = t.cnt_off + align16((kMaxSpecies + 1) * 4);
     t.total = t.flag_off + 16;
@@ -237,6 +237,7 @@ __device__ __forceinline__ void attempt_setup(const RuleArgs& rule, uint32_t sT,
         sSlow.xi = rule.xi;
         sSlow.sT = sT;
         sSlow.S1 = S1;
+        sSlow.gT = rule.T;
     }
 }
 
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
     uint8_t* glat = a.lat + static_cast<size_t>(r) * H * L;
     const uint32_t s32 = seed32(a.seeds[r]);
 
-    for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+    fill_pair_thresholds<ARITY>(reinterpret_cast<uint2*>(sT), a.rule.T, S1);
     attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
     tile_copy<true>(lat, glat, H, L, P);
     __syncthreads();
@@ -1090,7 +1091,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     const int woff = (Wh * P + 15) & ~15;
     uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
     // (256 bytes after the thresholds are reserved: block_smem's layout predates the static tables)
-    uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8);
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + woff + ((S1 * S1 * 8 + 15) & ~15) + 32 * 8);
     uint8_t* sScratch = reinterpret_cast<uint8_t*>(sCnt + kMaxSpecies + 1);  // 4 * P bytes (dummy box)
     __shared__ int sLast;
     __shared__ __align__(8) uint64_t sMbar;
@@ -1103,7 +1104,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
     if (SEAM && a.step) {
         const uint32_t s32 = seed32(a.seeds[r]);
         const int wy0 = ((ry0 - My) % H + H) % H, wx0 = ((rx0 - Mx) % L + L) % L;
-        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+        fill_pair_thresholds<ARITY>(reinterpret_cast<uint2*>(sT), a.rule.T, S1);
         attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
         SeamEntry* rows = reinterpret_cast<SeamEntry*>(
             (reinterpret_cast<uintptr_t>(sScratch) + 4 * P + 15) & ~static_cast<uintptr_t>(15));
@@ -1120,7 +1121,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         const uint32_t s32 = seed32(a.seeds[r]);
         const int wy0 = max(0, ry0 - My), wx0 = max(0, rx0 - Mx);
         const int wh = min(H, ry1 + My) - wy0, ww = min(L, rx1 + Mx) - wx0;
-        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+        fill_pair_thresholds<ARITY>(reinterpret_cast<uint2*>(sT), a.rule.T, S1);
         attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
         asm volatile("griddepcontrol.wait;" ::: "memory");
         if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
@@ -1134,7 +1135,7 @@ __global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
         const int wx0 = ((rx0 - Mx) % L + L) % L;
         const uint32_t mbar = smem_addr(&sMbar);
         // prologue: inputs that no earlier launch writes (rule, seeds, geometry)
-        for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+        fill_pair_thresholds<ARITY>(reinterpret_cast<uint2*>(sT), a.rule.T, S1);
         attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
         if (TAB && tid < 32) {
             BlockGeom gt;
@@ -1273,12 +1274,12 @@ __global__ void __launch_bounds__(1024) block_kernel_persistent(PersistArgs pa) 
     const int woff = (Whm * P + 15) & ~15;
     uint32_t* sT = reinterpret_cast<uint32_t*>(smem + woff);
     // (256 bytes after the thresholds are reserved: block_smem's layout predates the static tables)
-    uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + woff + ((S1 * S1 * 4 + 15) & ~15) + 32 * 8);
+    uint32_t* sCnt = reinterpret_cast<uint32_t*>(smem + woff + ((S1 * S1 * 8 + 15) & ~15) + 32 * 8);
     uint8_t* sScratch = reinterpret_cast<uint8_t*>(sCnt + kMaxSpecies + 1);
     __shared__ __align__(8) uint64_t sMbar;
 
     const uint32_t s32 = seed32(a.seeds[r]);
-    for (int i = tid; i < S1 * S1; i += nt) sT[i] = a.rule.T[i];
+    fill_pair_thresholds<ARITY>(reinterpret_cast<uint2*>(sT), a.rule.T, S1);
     attempt_setup<ARITY>(a.rule, smem_addr(sT), S1, P);
     for (int i = tid; i < P; i += nt) reinterpret_cast<uint32_t*>(sScratch)[i] = 0u;
     const uint32_t mbar = smem_addr(&sMbar);
