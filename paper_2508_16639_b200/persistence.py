@@ -14,6 +14,7 @@ checkpoint resumes bit-exactly without a streams.csv (the reference's MT19937 st
 from __future__ import annotations
 
 import os
+import re
 from dataclasses import dataclass, field
 from typing import List, Optional
 
@@ -57,11 +58,15 @@ def _split_csv(line):
     return line.split(",")
 
 
+_INT_RE = re.compile(r"-?[0-9]+\Z")
+
+
 def _parse_int(text, what):
-    t = text.strip() if False else text
-    if not t or not (t.lstrip("-").isdigit()) or (t.startswith("-") and len(t) == 1):
+    """persistence.cpp:39-45 (std::from_chars into int64): optional '-', ASCII digits only, the whole
+    field, in range."""
+    if not _INT_RE.match(text) or not (-(1 << 63) <= int(text) < (1 << 63)):
         raise FormatError("invalid integer '%s' for %s" % (text, what))
-    return int(t)
+    return int(text)
 
 
 def _parse_double(text, what):

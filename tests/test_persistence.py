@@ -92,3 +92,13 @@ def test_device_resume_from_checkpoint_is_bit_exact(escg, tmp_path):
     assert rest.state.current_mcs == 60
     assert np.array_equal(rest.state.lattice.cells, full.state.lattice.cells)
     assert rest.state.trace.counts[-1].tolist() == full.state.trace.counts[-1].tolist()
+
+
+def test_parse_int_follows_from_chars(escg):
+    from paper_2508_16639_b200 import persistence as P
+
+    assert P._parse_int("-12", "x") == -12 and P._parse_int("007", "x") == 7
+    for bad in ["", "-", "+5", " 5", "5 ", "1e3", "²", "9223372036854775808", "--1"]:
+        with pytest.raises(escg.FormatError):
+            P._parse_int(bad, "x")
+    assert P._parse_int("9223372036854775807", "x") == (1 << 63) - 1
