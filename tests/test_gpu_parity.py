@@ -541,3 +541,37 @@ def test_auto_kernel_choice(escg):
         assert eng.describe()["kernel"] == "tile"
     with escg.DeviceEngine(params(escg, 3200, 3200, 3, 1e-4, 0.1, 4, True), model) as eng:
         assert eng.describe()["kernel"] == "block"
+
+
+def _fnv1a_i32(cells):
+    h = 1469598103934665603
+    for b in np.ascontiguousarray(cells, "<i4").tobytes():
+        h = ((h ^ b) * 1099511628211) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def test_reference_simulate_dispatches_to_device_engine(escg, ref):
+    """INTEGRATION.md §1 compiled for real: the unmodified reference with the EngineMode::Device case
+    (oracle/device_patch.py) runs escg::simulate() on this engine through the C ABI; the result equals
+    this package's simulate() from the same MT19937-initialised lattice, bit for bit."""
+    import os
+    import subprocess
+
+    demo = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                        "escg_device_demo")
+    if not os.path.exists(demo):
+        pytest.skip("oracle/_ref/escg_device_demo not built (needs /root/reference at build time)")
+    L, H, mcs = 64, 48, 120
+    out = subprocess.run([demo, str(L), str(H), str(mcs)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    got = dict(kv.split("=") for kv in out.stdout.split())
+    init = ref.init_lattice(L, H, 3, 0.1, 77)
+    assert int(got["init_fnv"], 16) == _fnv1a_i32(init)
+    p = escg.SimParams(length=L, height=H, species=3, mobility=1e-3, empty_prob=0.1, seed=77, mcs_limit=mcs,
+                       print_frequency=1000000)
+    res = escg.simulate(p, escg.make_circulant(3, [1]), escg.EngineMode.Serial,
+                        resume_from=escg.RunState(lattice=escg.Lattice(L, H, init), current_mcs=0))
+    assert int(got["status"]) == int(res.status) and int(got["mcs"]) == res.state.current_mcs
+    assert int(got["records"]) == len(res.state.trace.counts)
+    assert int(got["total"]) == L * H
+    assert int(got["final_fnv"], 16) == _fnv1a_i32(res.state.lattice.cells)
