@@ -265,7 +265,9 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
     const double kOverheadCells = 40000.0;  // launch + window load/store, measured on B200
+    const int kforce = std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0;  // experiments
     for (int k = 1; k <= kmax; ++k) {
+        if (kforce > 0 && k != kforce) continue;
         for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
             for (int nbx = 1; nbx <= std::min(ux, 128); ++nbx) {
                 const int bh = ((uy + nby - 1) / nby) * 4 + std::max(0, ry_extra),
