@@ -253,8 +253,9 @@ size_t block_smem(int bh, int bw, int S1, int k, int* pitch, int seam_np = 0) {
 // when L allows (TMA rows, NARROW pairs), and k MCS per launch (temporal blocking).  Model per MCS:
 // waves x (mean valid area over the 4k phases + launch/load overhead / k), in cell units.
 void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
-    // CTAs resident per SM at h->threads threads and <= 64 registers/thread (1024 → 1, 512 → 2)
-    const int cta_per_sm = h->threads <= 512 ? 2 : 1;
+    // CTAs resident per SM by registers (65536 per SM, allocated in units of 8 per thread)
+    const int regs = (escgd::block_kernel_registers(h->arity) + 7) / 8 * 8;
+    const int cta_per_sm = std::max(1, std::min(2, 65536 / std::max(1, regs * h->threads)));
     sms *= cta_per_sm;
     smem_cap = std::min(smem_cap, (228 * 1024) / cta_per_sm - 1024);
     const int cu = (h->L % 16 == 0) ? 16 : ((h->L % 8 == 0) ? 8 : 4);
@@ -300,11 +301,10 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     for (int i = 0; i < bnbx; ++i) bw = std::max(bw, cols[i + 1] - cols[i]);
     h->smem = static_cast<int>(block_smem(bh, bw, h->S1, bk, &h->P, h->seam_np));
     {
-        // items (tile pairs) per thread per phase: below ~3.5 the per-phase geometry is a large share
-        // of a warp's work and a table built once per launch pays (L=3200: +3.5%); above it the
-        // uniform-register recomputation keeps the item loop's registers free (L=16384: table -4.5%)
-        const double items = ((bh + 2.0 * escgd::margin_rows(bk)) / 4.0) * ((bw + 2.0 * escgd::margin_cols(bk)) / 8.0);
-        h->phase_table = items / h->threads < 3.5 ? 1 : 0;
+        // per-launch phase-geometry table: with 640-thread CTAs (96 registers) it wins at every size
+        // measured (L=1000 +6%, 2048 +7%, 3200 +5%, 16384 +2%); the recomputing path stays for
+        // comparison (ESCG_PHASE_TABLE=0)
+        h->phase_table = 1;
         if (const char* pt = std::getenv("ESCG_PHASE_TABLE")) h->phase_table = std::atoi(pt) ? 1 : 0;
     }
     h->bh_max = bh;
@@ -813,10 +813,13 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             h->threads = tile_threads;
         } else {
             h->lat[1].alloc(static_cast<size_t>(h->N) * n_replicas);
-            // lattices far beyond one CTA per SM stream through many waves: two 512-thread CTAs per
-            // SM overlap one CTA's load/barrier phases with the other's attempts (measured, L=16384)
-            h->threads = h->N >= (int64_t{64} << 20) ? 512 : 1024;
-            if (const char* tv = std::getenv("ESCG_BLOCK_THREADS")) h->threads = std::atoi(tv) == 512 ? 512 : 1024;
+            // 640 threads per CTA at up to 96 registers (the kernel's launch bound): fewer warps, no
+            // spills — faster than 1024 x 64 registers and than 2 x 512 per SM at every size measured
+            h->threads = escgd::kBlockThreads;
+            if (const char* tv = std::getenv("ESCG_BLOCK_THREADS")) {  // experiments: fewer threads
+                const int t = std::atoi(tv);
+                if (t >= 256 && t <= escgd::kBlockThreads && t % 32 == 0) h->threads = t;
+            }
             int kmax = escgd::kMaxBlockMcs;
             if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
             if (bs) kmax = bs->kmcs;  // chunks may not outgrow the band's halo

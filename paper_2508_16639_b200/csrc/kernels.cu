@@ -1062,7 +1062,7 @@ __device__ void load_window_bytes(uint8_t* win, const uint8_t* src, int H, int L
 }
 
 template <int ARITY, int BMODE, bool BF, bool TAB>
-__global__ void __launch_bounds__(1024) block_kernel(BlockArgs a) {
+__global__ void __launch_bounds__(kBlockThreads) block_kernel(BlockArgs a) {
     constexpr bool REFLECT = BMODE == 1, SEAM = BMODE == 2;
     extern __shared__ __align__(128) uint8_t smem[];
     // Programmatic dependent launch: let the next launch's CTAs start their prologue as soon as SMs
@@ -1622,6 +1622,15 @@ static cudaError_t block_launch_t(const BlockArgs& a, int nrep, int threads, cud
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k, a);
+}
+
+// Registers per thread of the periodic block kernel (the launch bound decides them).
+int block_kernel_registers(int arity) {
+    cudaFuncAttributes fa{};
+    const void* f = arity == 8 ? reinterpret_cast<const void*>(block_kernel<8, 0, false, false>)
+                               : reinterpret_cast<const void*>(block_kernel<4, 0, false, false>);
+    if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 64;
+    return fa.numRegs;
 }
 
 // Concurrent tile-kernel CTAs (one per replica) the device holds at this CTA shape.

@@ -19,6 +19,9 @@ constexpr int kTileR0 = 2;
 constexpr int kTileC0 = 4;
 constexpr int kMaxSpecies = 64;
 constexpr int kMaxDevices = 64;
+// Block-kernel CTA size = its launch bound: 640 threads → up to 96 registers per thread, no spills
+// (measured faster than 1024 x 64 registers and 2 x 512 per SM).
+constexpr int kBlockThreads = 640;
 
 struct RuleArgs {
     uint32_t xm, xi;       // X_mig, X_int
@@ -123,6 +126,7 @@ cudaError_t launch_block(const BlockArgs& a, int nrep, int threads, cudaStream_t
 cudaError_t launch_block_persistent(const PersistArgs& a, int nrep, int threads, cudaStream_t s);
 int block_persistent_capacity(int arity, int threads, int smem_bytes, int device);
 int tile_capacity(int arity, int flux, int H, int L, int threads, int smem_bytes, int device);
+int block_kernel_registers(int arity);
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
 cudaError_t launch_u8_to_i32(const uint8_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_i32_to_u8(const int32_t* src, uint8_t* dst, int64_t n, int S, int* bad, cudaStream_t s);
