@@ -502,6 +502,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.narrow = h->narrow;
         a.record = 1;
         a.smem_bytes = h->smem;
+        a.one_per_sm = escgd::tile_one_per_sm(h->smem) ? 1 : 0;
         CK(escgd::launch_tile(a, h->nrep, h->threads, h->stream));
         launches = 1;
     } else if (h->persist) {
@@ -764,9 +765,10 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             const int64_t items = ((h->H + 3) / 4) * (int64_t)((h->L + 7) / 8);
             int64_t tt = (items * 2 / 5) / 32 * 32;
             tt = tt > 448 ? 512 : std::max<int64_t>(64, tt);
-            tile_threads = static_cast<int>(tt);
+            const int cap = escgd::tile_one_per_sm(tbytes) ? escgd::kTileThreadsOne : escgd::kTileThreadsTwo;
+            tile_threads = static_cast<int>(std::min<int64_t>(tt, cap));
             if (const char* tv = std::getenv("ESCG_TILE_THREADS"))
-                tile_threads = std::max(32, std::min(512, (std::atoi(tv) + 31) / 32 * 32));
+                tile_threads = std::max(32, std::min(cap, (std::atoi(tv) + 31) / 32 * 32));
         }
         int choice = kernel;
         if (choice == ESCG_KERNEL_AUTO) {
@@ -963,6 +965,7 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
             a.narrow = h->narrow;
             a.record = 0;
             a.smem_bytes = h->smem;
+            a.one_per_sm = escgd::tile_one_per_sm(h->smem) ? 1 : 0;
             // per-replica limit: all replicas advance by n_mcs from their own MCS; the kernel
             // reads mcs[r] and runs to mcs_limit, so stage limit = mcs + n per replica by
             // shifting: launch once per distinct starting MCS.

@@ -373,8 +373,12 @@ __device__ void tile_copy(uint8_t* lat, uint8_t* glat, int H, int L, int P) {
     }
 }
 
-template <int ARITY, int MODE, bool BF>
-__global__ void __launch_bounds__(512, 2) tile_kernel(TileArgs a) {
+// Launch shapes of the tile kernel (measured on B200 ensembles): lattices whose shared memory allows
+// two CTAs per SM use <= 384 threads at <= 80 registers (L=200 x 296 replicas +3%, L=100 +2% over
+// 512 x 64); larger ones, one CTA per SM anyway, use <= 512 threads at up to 128 registers (L=400 +5%).
+template <int ARITY, int MODE, bool BF, bool ONE_PER_SM>
+__global__ void __launch_bounds__(ONE_PER_SM ? kTileThreadsOne : kTileThreadsTwo, ONE_PER_SM ? 1 : 2)
+    tile_kernel(TileArgs a) {
     constexpr bool REFLECT = MODE == kModeReflect;
     extern __shared__ __align__(128) uint8_t smem[];
     const int H = a.H, L = a.L, P = a.P, S1 = a.S + 1;
@@ -1565,7 +1569,9 @@ cudaError_t launch_count(const uint8_t* lat, int64_t n, int nrep, int S, unsigne
 
 template <int ARITY, int MODE>
 static cudaError_t tile_launch_t(const TileArgs& a, int nrep, int threads, cudaStream_t s) {
-    auto k = a.rule.wide_bf ? tile_kernel<ARITY, MODE, true> : tile_kernel<ARITY, MODE, false>;
+    const bool one = a.one_per_sm != 0;
+    auto k = a.rule.wide_bf ? (one ? tile_kernel<ARITY, MODE, true, true> : tile_kernel<ARITY, MODE, true, false>)
+                            : (one ? tile_kernel<ARITY, MODE, false, true> : tile_kernel<ARITY, MODE, false, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, a.smem_bytes);
     if (e != cudaSuccess) return e;
     k<<<nrep, threads, a.smem_bytes, s>>>(a);
@@ -1634,17 +1640,20 @@ int block_kernel_registers(int arity) {
 }
 
 // Concurrent tile-kernel CTAs (one per replica) the device holds at this CTA shape.
+template <bool ONE>
+static const void* tile_fn(int arity, int mode) {
+    if (arity == 8)
+        return mode == kModeReflect ? reinterpret_cast<const void*>(tile_kernel<8, kModeReflect, false, ONE>)
+               : mode == kModeSeam  ? reinterpret_cast<const void*>(tile_kernel<8, kModeSeam, false, ONE>)
+                                    : reinterpret_cast<const void*>(tile_kernel<8, kModePeriodic, false, ONE>);
+    return mode == kModeReflect ? reinterpret_cast<const void*>(tile_kernel<4, kModeReflect, false, ONE>)
+           : mode == kModeSeam  ? reinterpret_cast<const void*>(tile_kernel<4, kModeSeam, false, ONE>)
+                                : reinterpret_cast<const void*>(tile_kernel<4, kModePeriodic, false, ONE>);
+}
+
 int tile_capacity(int arity, int flux, int H, int L, int threads, int smem_bytes, int device) {
     const int mode = !flux ? kModeReflect : ((H % 4 == 0 && L % 4 == 0) ? kModePeriodic : kModeSeam);
-    const void* f = nullptr;
-    if (arity == 8)
-        f = mode == kModeReflect ? reinterpret_cast<const void*>(tile_kernel<8, kModeReflect, false>)
-            : mode == kModeSeam  ? reinterpret_cast<const void*>(tile_kernel<8, kModeSeam, false>)
-                                 : reinterpret_cast<const void*>(tile_kernel<8, kModePeriodic, false>);
-    else
-        f = mode == kModeReflect ? reinterpret_cast<const void*>(tile_kernel<4, kModeReflect, false>)
-            : mode == kModeSeam  ? reinterpret_cast<const void*>(tile_kernel<4, kModeSeam, false>)
-                                 : reinterpret_cast<const void*>(tile_kernel<4, kModePeriodic, false>);
+    const void* f = tile_one_per_sm(smem_bytes) ? tile_fn<true>(arity, mode) : tile_fn<false>(arity, mode);
     int per_sm = 0, sms = 0;
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) return 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, threads, smem_bytes) != cudaSuccess) return 0;

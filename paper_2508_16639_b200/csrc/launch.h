@@ -22,6 +22,10 @@ constexpr int kMaxDevices = 64;
 // Block-kernel CTA size = its launch bound: 640 threads → up to 96 registers per thread, no spills
 // (measured faster than 1024 x 64 registers and 2 x 512 per SM).
 constexpr int kBlockThreads = 640;
+// Tile-kernel launch shapes (kernels.cu tile_kernel): two CTAs per SM when the lattice's shared
+// memory allows it (<= 384 threads, <= 80 registers), else one (<= 512 threads, <= 128 registers).
+constexpr int kTileThreadsTwo = 384, kTileThreadsOne = 512;
+inline bool tile_one_per_sm(int smem_bytes) { return smem_bytes > (228 * 1024) / 2 - 1024 - 1024; }
 
 struct RuleArgs {
     uint32_t xm, xi;       // X_mig, X_int
@@ -56,6 +60,7 @@ struct TileArgs {
     int narrow;       // draw format
     int record;       // 1: record/check loop (escg_dev_run); 0: advance to run.mcs_limit
     int smem_bytes;
+    int one_per_sm;   // launch shape (tile_one_per_sm(smem_bytes))
 };
 
 struct BlockArgs {
