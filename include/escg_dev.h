@@ -147,7 +147,8 @@ ESCG_API int escg_dev_last_timing(escg_dev* h, double* ms, int64_t* launches);
 ESCG_API int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t* threads, int32_t* smem_bytes);
 
 /* Draw format chosen for this engine: 0 WIDE (32-bit attempt words), 1 NARROW (16-bit words, one
- * draw per tile pair) — DESIGN.md §RNG; the oracle needs it to replay the schedule. */
+ * draw per tile pair), 2 | K << 8 SLICED (bit-plane draws shared by 32 tiles, K action planes; the
+ * bit-sliced block kernel) — DESIGN.md §RNG; the oracle needs it to replay the schedule. */
 ESCG_API int escg_dev_draw_format(escg_dev* h, int32_t* narrow);
 
 /* Block kernel mode: MCS per chunk (temporal blocking; 1 for the tile kernel) and whether a run

@@ -398,7 +398,7 @@ EXPORT void orc_philox(const uint32_t* ctr_in, const uint32_t* key_in, uint32_t*
  *   c1   = mcs bits 0..31
  *   c2   = mcs bits 32..47 | domain << 16 | phase << 20 | attempt << 24
  *   c3   = seed32 = u32(seed) ^ murmur_finalize(u32(seed >> 32))  (= u32(seed) for seeds < 2^32) */
-enum { DOM_STEP = 0, DOM_REFINE = 1, DOM_ROUND = 2, DOM_INIT = 3 };
+enum { DOM_STEP = 0, DOM_REFINE = 1, DOM_ROUND = 2, DOM_INIT = 3, DOM_SLICE = 4, DOM_SLICE_REF = 5 };
 static const uint32_t kKey0 = 0xA4093822u, kKey1 = 0x299F31D0u;
 
 EXPORT uint32_t orc_seed32(uint64_t seed) {
@@ -503,7 +503,15 @@ EXPORT void orc_crs_init(int length, int height, int species, double empty_prob,
  *         tile half h = (tx>>1)&1 uses words 2h, 2h+1; attempt a uses 16-bit half (a&1) of word
  *         2h+(a>>1): bits [0,LB) direction/cell, action x = (half >> LB) << (32-(16-LB))
  *         | (REFINE(tile,p,a).x & (2^(16+LB)-1)).
- * In both formats the action word is a uniform 32-bit value assembled from disjoint Philox bits, so
+ *  SLICED (fmt = 2 | K << 8; periodic, VN4, L % 128 == 0, H % 4 == 0, X_mig >= 2^32 - 2^(32-K)):
+ *         bit-plane draws shared by the 32 same-colour tiles whose anchor (top-left) cell (y, x)
+ *         = (2ty - oy, 2tx - ox) mod (H, L) lies in columns [128g, 128g + 128) of tile row ty:
+ *         item id c0 = ty * (L / 128) + g, lane l = (x mod 128) >> 2.  Words W[4j .. 4j+3] =
+ *         SLICE draw j (attempt field j) for j < 4 + K; attempt a reads bit l of W[4a] (cell row),
+ *         W[4a+1] (cell column), W[4a+2] | W[4a+3] << 1 (direction) and of W[16 + aK + i], i < K,
+ *         as bit 31-i of the action word; its low 32-K bits are word a of SLICE_REF draw
+ *         (c0 = item, attempt field l).
+ * In every format the action word is a uniform 32-bit value assembled from disjoint Philox bits, so
  * the rule sees exactly the reference's action distribution. */
 static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a, uint32_t* low, uint32_t* hi_part,
                              int* hi_shift) {
@@ -524,7 +532,7 @@ static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a
  * colour have disjoint footprints, so the order within a phase is immaterial; this loop is the
  * sequential definition the GPU kernels must reproduce bit-for-bit.  Returns 0 / 5 / 2. */
 EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int arity, int flux,
-                       const double* dom, double mobility, uint64_t seed, int64_t mcs0, int64_t n_mcs, int narrow) {
+                       const double* dom, double mobility, uint64_t seed, int64_t mcs0, int64_t n_mcs, int fmt) {
     orc_ctx c;
     const int periodic = flux != 0;
     const int db = arity == 8 ? 3 : 2;
@@ -532,7 +540,9 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
     if (periodic && (length < 4 || height < 4)) return 2;
     int seam_y = -1, seam_x = -1;
     const int ncy = periodic ? crs_axis(height, &seam_y) : 2, ncx = periodic ? crs_axis(length, &seam_x) : 2;
+    const int narrow = (fmt & 0xFF) == 1, sliced = (fmt & 0xFF) == 2, K = fmt >> 8;
     if (narrow && (ncy != 2 || ncx != 2 || length % 8 != 0)) return 2;
+    if (sliced && (ncy != 2 || ncx != 2 || length % 128 != 0 || arity != 4 || K < 1 || K > 24)) return 2;
     orc_ctx_make(&c, length, height, species, arity, flux, dom, mobility);
     for (int64_t mcs = mcs0; mcs < mcs0 + n_mcs; ++mcs) {
         int oy, ox, perm[9];
@@ -548,16 +558,38 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
                     const uint32_t tile = (uint32_t)ty * (uint32_t)tx_n + (uint32_t)tx;
                     const uint32_t sid = narrow ? (uint32_t)ty * (uint32_t)tq + (uint32_t)(tx >> 2) : tile;
                     const int h = (tx >> 1) & 1;
-                    uint32_t w[4];
-                    crs_draw(seed, sid, (uint64_t)mcs, DOM_STEP, (uint32_t)p, 0, w);
+                    uint32_t w[4], sw[4 * (4 + 24)], srf[4];
+                    int lane = 0;
+                    if (sliced) {
+                        const int ax = ((2 * tx - ox) % length + length) % length;
+                        const uint32_t item = (uint32_t)ty * (uint32_t)(length / 128) + (uint32_t)(ax >> 7);
+                        lane = (ax & 127) >> 2;
+                        for (int j = 0; j < 4 + K; ++j)
+                            crs_draw(seed, item, (uint64_t)mcs, DOM_SLICE, (uint32_t)p, (uint32_t)j, sw + 4 * j);
+                        crs_draw(seed, item, (uint64_t)mcs, DOM_SLICE_REF, (uint32_t)p, (uint32_t)lane, srf);
+                    } else {
+                        crs_draw(seed, sid, (uint64_t)mcs, DOM_STEP, (uint32_t)p, 0, w);
+                    }
                     for (int a = 0; a < 4; ++a) {
                         uint32_t rf[4], low, hi_part;
                         int hi_shift;
-                        crs_attempt_bits(narrow, lb, w, h, a, &low, &hi_part, &hi_shift);
-                        const int dir = (int)(low & (uint32_t)(arity - 1));
-                        const int dy = (int)((low >> db) & 1u), dx = (int)((low >> (db + 1)) & 1u);
-                        crs_draw(seed, tile, (uint64_t)mcs, DOM_REFINE, (uint32_t)p, (uint32_t)a, rf);
-                        const uint32_t x = (hi_part << hi_shift) | (rf[0] & ((1u << hi_shift) - 1u));
+                        uint32_t x;
+                        int dir, dy, dx;
+                        if (sliced) {
+                            dy = (int)((sw[4 * a] >> lane) & 1u);
+                            dx = (int)((sw[4 * a + 1] >> lane) & 1u);
+                            dir = (int)(((sw[4 * a + 2] >> lane) & 1u) | (((sw[4 * a + 3] >> lane) & 1u) << 1));
+                            uint32_t hi = 0;
+                            for (int i = 0; i < K; ++i) hi = (hi << 1) | ((sw[16 + a * K + i] >> lane) & 1u);
+                            x = (hi << (32 - K)) | (srf[a] & ((1u << (32 - K)) - 1u));
+                        } else {
+                            crs_attempt_bits(narrow, lb, w, h, a, &low, &hi_part, &hi_shift);
+                            dir = (int)(low & (uint32_t)(arity - 1));
+                            dy = (int)((low >> db) & 1u);
+                            dx = (int)((low >> (db + 1)) & 1u);
+                            crs_draw(seed, tile, (uint64_t)mcs, DOM_REFINE, (uint32_t)p, (uint32_t)a, rf);
+                            x = (hi_part << hi_shift) | (rf[0] & ((1u << hi_shift) - 1u));
+                        }
                         int y = 2 * ty - oy + dy, xc = 2 * tx - ox + dx;
                         if (periodic) {
                             /* the missing half of an odd axis' last tile: no attempt */

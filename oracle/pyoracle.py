@@ -180,11 +180,13 @@ class Oracle:
         return cells
 
     def crs_run(self, cells, length, height, dom, mobility, seed, mcs0, n_mcs, arity=4, flux=True, narrow=False):
+        """`narrow`: draw format — False/True (WIDE/NARROW) or the engine's draw code
+        (DeviceEngine.draw_code(): 0 WIDE, 1 NARROW, 2 | K << 8 SLICED)."""
         species = int(round(np.sqrt(np.asarray(dom).size)))
         cells = np.ascontiguousarray(cells, np.int32).copy()
         rc = self.lib.orc_crs_run(cells, length, height, species, arity, int(flux),
                                   np.ascontiguousarray(dom, np.float64).ravel(), mobility, seed, mcs0, n_mcs,
-                                  int(bool(narrow)))
+                                  narrow if isinstance(narrow, int) and not isinstance(narrow, bool) else int(bool(narrow)))
         if rc:
             raise RuntimeError("oracle crs error %d" % rc)
         return cells

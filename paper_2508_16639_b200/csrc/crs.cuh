@@ -208,7 +208,7 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
 }
 
 // REFINE-domain word of attempt a of `tile` (exact action completion; rare).
-__device__ __noinline__ uint32_t refine_word(uint32_t tile, int a, uint32_t c1, uint32_t c2, uint32_t c3) {
+static __device__ __noinline__ uint32_t refine_word(uint32_t tile, int a, uint32_t c1, uint32_t c2, uint32_t c3) {
     return philox(tile, c1, (c2 ^ kStepToRefine) | (static_cast<uint32_t>(a) << 24), c3).x;
 }
 

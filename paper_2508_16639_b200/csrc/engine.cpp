@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -182,7 +183,9 @@ struct escg_dev {
     int smem = 0;
     int P = 0;
     int nby = 1, nbx = 1;
-    int narrow = 0;  // draw format
+    int narrow = 0;  // draw format: 0 WIDE, 1 NARROW, 2 SLICED (bit-sliced block kernel)
+    int K = 0;       // SLICED: action bit planes
+    int npl = 2;     // SLICED: species-code bit planes
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
     int bh_max = 0, bw_max = 0;
@@ -202,6 +205,7 @@ struct escg_dev {
     std::vector<int64_t> mcs;  // host mirror per replica
     std::vector<int> cur;      // block path: buffer holding replica r's lattice
     DevBuf<uint8_t> lat[2];
+    DevBuf<uint32_t> pl[2];  // SLICED: bit-plane lattices during run/advance (slice.cu)
     DevBuf<uint64_t> d_seeds, d_last;
     DevBuf<uint32_t> d_T;
     DevBuf<int64_t> d_mcs, d_nrec, d_tsteps;
@@ -315,6 +319,71 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     CK(cudaMemcpy(h->d_cols.p, cols.data(), sizeof(int) * cols.size(), cudaMemcpyHostToDevice));
 }
 
+// Bit-sliced block decomposition (slice.cu): row splits at multiples of 4, column blocks of whole
+// 128-column groups (block i covers [128 s_i + 64, 128 s_{i+1} + 64), its window the s_{i+1} - s_i + 1
+// groups from s_i), k MCS per launch.  Work per CTA and MCS ~ (rows + 12k) x window width: the
+// bit-parallel items cover whole groups whether or not their columns are valid.
+void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
+    const int regs = (escgd::slice_kernel_registers(h->npl, h->K) + 7) / 8 * 8;
+    const int cta_per_sm = std::max(1, std::min(4, 65536 / std::max(1, regs * escgd::kSliceThreads)));
+    sms *= cta_per_sm;
+    const int GL = h->L / 128, uy = h->H / 4;
+    double best = 1e300;
+    int bnby = 1, bnbx = 1, bk = 1;
+    double overhead = 20000.0;  // launch + window load/store, in cell units
+    if (const char* o = std::getenv("ESCG_SLICE_OVERHEAD")) overhead = std::atof(o);
+    const int kforce = std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0;
+    for (int k = 1; k <= kmax; ++k) {
+        if (kforce > 0 && k != kforce) continue;
+        for (int nbx = 1; nbx <= GL; ++nbx) {
+            const int Gw = (GL + nbx - 1) / nbx + 1;
+            if (Gw > 32) continue;  // a warp holds whole window rows (lanes = groups)
+            // lanes of a warp: floor(32 / Gw) tile rows x Gw groups; the rest idle through the phase
+            const double lanes = 32.0 / ((32 / Gw) * Gw);
+            for (int nby = 1; nby <= std::min(uy, 512); ++nby) {
+                const int bh = ((uy + nby - 1) / nby) * 4;
+                const size_t smem = static_cast<size_t>(bh + 2 * escgd::margin_rows(k)) *
+                                    escgd::slice_row_words(h->npl, Gw) * 4;
+                if (smem > static_cast<size_t>(smem_cap)) continue;
+                const int64_t ctas = static_cast<int64_t>(nby) * nbx * h->nrep;
+                const int64_t waves = (ctas + sms - 1) / sms;
+                const double area = (bh + 12.0 * k + 3.0) * 128.0 * Gw * lanes;
+                const double cost = static_cast<double>(waves) * (area + overhead / k);
+                if (cost < best * 0.999) {
+                    best = cost;
+                    bnby = nby;
+                    bnbx = nbx;
+                    bk = k;
+                }
+            }
+        }
+    }
+    if (const char* sp = std::getenv("ESCG_SLICE_SPLIT")) {  // tests/experiments: "nby,nbx"
+        int y = 0, x = 0;
+        if (std::sscanf(sp, "%d,%d", &y, &x) == 2 && y >= 1 && y <= uy && x >= 1 && x <= GL) {
+            bnby = y;
+            bnbx = x;
+        }
+    }
+    h->nby = bnby;
+    h->nbx = bnbx;
+    h->kmcs = bk;
+    std::vector<int> rows(bnby + 1), cols(bnbx + 1);
+    for (int i = 0; i <= bnby; ++i) rows[i] = static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
+    for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(GL) * i / bnbx);
+    int bh = 0, gw = 0;
+    for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
+    for (int i = 0; i < bnbx; ++i) gw = std::max(gw, cols[i + 1] - cols[i] + 1);
+    h->smem = (bh + 2 * escgd::margin_rows(bk)) * escgd::slice_row_words(h->npl, gw) * 4;
+    h->bh_max = bh;
+    h->bw_max = 128 * (gw - 1);
+    h->threads = escgd::kSliceThreads;
+    h->d_rows.alloc(rows.size());
+    h->d_cols.alloc(cols.size());
+    CK(cudaMemcpy(h->d_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(h->d_cols.p, cols.data(), sizeof(int) * cols.size(), cudaMemcpyHostToDevice));
+}
+
 escgd::RuleArgs rule_args(escg_dev* h) {
     const int LB = h->arity == 8 ? 5 : 4;
     // WIDE rule form (crs.cuh rule_wide, a kernel template parameter): branch-free unless
@@ -410,6 +479,8 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.acc = h->d_acc.p;
     a.ticket = h->d_ticket.p;
     a.smem_bytes = h->smem;
+    a.K = h->K;
+    a.npl = h->npl;
     a.step = 1;
     int64_t launches = 0;
     for (int64_t done = 0; done < n;) {
@@ -417,12 +488,17 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
         const int par = static_cast<int>(launch_no & 1);
         a.src = h->lat[par].p;
         a.dst = h->lat[1 - par].p;
+        a.psrc = h->pl[par].p;
+        a.pdst = h->pl[1 - par].p;
         a.dst_index = 1 - par;
         a.mcs = t + done;
         a.nmcs = k;
         done += k;
         a.count = (count_last && done == n) ? 1 : 0;
-        CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
+        if (h->narrow == 2)
+            CK(escgd::launch_slice(a, h->nrep, h->stream));
+        else
+            CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
         ++launch_no;
         ++launches;
     }
@@ -549,8 +625,19 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.acc = h->d_acc.p;
         a.ticket = h->d_ticket.p;
         a.smem_bytes = h->smem;
-        CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
-        ++launches;
+        if (h->narrow == 2) {
+            // SLICED: the run works on bit planes; the record at the start counts them
+            CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+            a.psrc = h->pl[0].p;
+            a.pdst = h->pl[1].p;
+            a.K = h->K;
+            a.npl = h->npl;
+            CK(escgd::launch_slice(a, h->nrep, h->stream));
+            launches += 2;
+        } else {
+            CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
+            ++launches;
+        }
         // Poll the device status every few chunks so a stasis/stop does not leave thousands of
         // no-op launches queued; the poll lags one chunk behind the enqueue front.
         int32_t* hstat = h->h_status;
@@ -575,6 +662,12 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
                 CK(cudaEventRecord(polled, h->stream));
                 poll_pending = true;
             }
+        }
+        if (h->narrow == 2) {
+            // back to bytes: the plane buffer named by the last record (cur = 2 + index)
+            CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, h->d_cur.p, 0, h->lat[0].p, h->H, h->L, h->npl,
+                                         h->nrep, h->stream));
+            ++launches;
         }
     }
     timed_end(h, launches);
@@ -803,6 +896,23 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 if (std::strcmp(f, "narrow") == 0 && periodic4 && h->L % 8 == 0) h->narrow = 1;
             }
         }
+        // SLICED (bit-sliced block kernel, slice.cu): periodic von Neumann lattices with L % 128 == 0,
+        // S <= 7, single-band engines, when at least 6 leading bits of X_mig are ones: K (even, <= 16,
+        // <= those bits) action planes make every word with a zero among its top K bits a certain
+        // migration.  Chosen by default from 8 leading ones (P(migration) >= 0.996).
+        {
+            int lead = 0;
+            while (lead < 32 && ((h->th.xm >> (31 - lead)) & 1u)) ++lead;
+            const bool ok = choice == ESCG_KERNEL_BLOCK && !bs && periodic4 && h->arity == 4 && h->L % 128 == 0 &&
+                            h->S <= 7 && lead >= 6;
+            bool use = ok && lead >= 8;
+            if (const char* f = std::getenv("ESCG_DRAW_FORMAT")) use = ok && std::strcmp(f, "sliced") == 0;
+            if (use) {
+                h->narrow = 2;
+                h->K = std::min(lead, escgd::kSliceMaxK) & ~1;
+                h->npl = h->S <= 3 ? 2 : 3;
+            }
+        }
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         CK(cudaEventCreate(&h->ev0));
         CK(cudaEventCreate(&h->ev1));
@@ -825,7 +935,14 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             int kmax = escgd::kMaxBlockMcs;
             if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
             if (bs) kmax = bs->kmcs;  // chunks may not outgrow the band's halo
-            plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
+            if (h->narrow == 2) {
+                plan_slices(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
+                const size_t words = static_cast<size_t>(h->H) * h->npl * (h->L / 128) * 4 * n_replicas;
+                h->pl[0].alloc(words);
+                h->pl[1].alloc(words);
+            } else {
+                plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
+            }
             h->d_cur.alloc(n_replicas);
             // persistent cooperative mode: every CTA co-resident, 16-aligned columns (TMA rows and
             // vector stores) and a window that wraps at most once
@@ -835,7 +952,7 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             const bool geom_ok = h->L % 16 == 0 && h->bw_max % 16 == 0 &&
                                  h->bh_max + 2 * escgd::margin_rows(h->kmcs) <= h->H &&
                                  h->bw_max + 2 * escgd::margin_cols(h->kmcs) <= h->L;
-            if (!env_off && geom_ok && h->wrap_rows && h->flux) {
+            if (!env_off && geom_ok && h->wrap_rows && h->flux && h->narrow != 2) {
                 const int cap = escgd::block_persistent_capacity(h->arity, h->threads, h->smem, device);
                 h->persist = h->nby * h->nbx * n_replicas <= cap;
             }
@@ -1003,7 +1120,16 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
             const int64_t t0 = h->mcs[0];
             int64_t launch_no = 0;
             timed_begin(h);
-            launches = enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
+            if (h->narrow == 2 && n_mcs > 0) {
+                CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+                launches = 1 + enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
+                CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, static_cast<int>(launch_no & 1),
+                                             h->lat[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+                ++launches;
+                launch_no = 0;  // the lattice is back in byte buffer 0
+            } else if (h->narrow != 2) {
+                launches = enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
+            }
             timed_end(h, launches);
             for (int r = 0; r < h->nrep; ++r) {
                 h->mcs[r] += n_mcs;
@@ -1023,7 +1149,9 @@ int escg_dev_run(escg_dev* h, int64_t mcs_limit, int64_t interval, uint32_t stop
         const std::vector<int64_t> start(h->mcs);
         run_impl(h, mcs_limit, interval, stop_flags, tracked_species, record_trace != 0, status_out);
         (void)start;
-        if (h->kernel == ESCG_KERNEL_BLOCK)
+        if (h->kernel == ESCG_KERNEL_BLOCK && h->narrow == 2)
+            std::fill(h->cur.begin(), h->cur.end(), 0);  // converted back into byte buffer 0
+        else if (h->kernel == ESCG_KERNEL_BLOCK)
             CK(cudaMemcpy(h->cur.data(), h->d_cur.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost));
     });
 }
@@ -1324,7 +1452,7 @@ int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
 int escg_dev_draw_format(escg_dev* h, int32_t* narrow) {
     return guarded([&] {
         if (!h || !narrow) config_error("null argument");
-        *narrow = h->narrow;
+        *narrow = h->narrow == 2 ? (2 | (h->K << 8)) : h->narrow;
     });
 }
 

@@ -89,6 +89,13 @@ struct BlockArgs {
     unsigned long long* acc;  // [rep][S+1] cross-CTA accumulators (zero between records)
     unsigned int* ticket;     // [rep]
     int smem_bytes;
+    // bit-sliced path (narrow == 2, slice.cu): the lattice as NPL bit planes [rep][H][NPL][L/128][4]
+    // u32 (word q of group g holds columns 128g + 4b + q in bit b); col_split then holds group
+    // splits (block i covers columns [128 s_i + 64, 128 s_{i+1} + 64))
+    const uint32_t* psrc;
+    uint32_t* pdst;
+    int K;    // SLICED action planes
+    int npl;  // bit planes (species code bits)
 };
 
 // Persistent cooperative block kernel: the whole run/advance in one launch (all CTAs co-resident).
@@ -133,6 +140,17 @@ int block_persistent_capacity(int arity, int threads, int smem_bytes, int device
 int tile_capacity(int arity, int flux, int H, int L, int threads, int smem_bytes, int device);
 int block_kernel_registers(int arity);
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
+// bit-sliced path (slice.cu)
+constexpr int kSliceThreads = 256;
+constexpr int kSliceMaxK = 16;
+cudaError_t launch_slice(const BlockArgs& a, int nrep, cudaStream_t s);
+int slice_row_words(int npl, int gw);  // shared-memory words per window row (padded)
+int slice_kernel_registers(int npl, int K);
+// u8 lattice <-> bit planes for every replica; from_planes picks plane buffer cur[r] - 2 when cur
+// is given (replicas with cur[r] < 2 are skipped), else `buf`
+cudaError_t launch_to_planes(const uint8_t* lat, uint32_t* pl, int H, int L, int npl, int nrep, cudaStream_t s);
+cudaError_t launch_from_planes(const uint32_t* pl0, const uint32_t* pl1, const int32_t* cur, int buf, uint8_t* lat,
+                               int H, int L, int npl, int nrep, cudaStream_t s);
 cudaError_t launch_u8_to_i32(const uint8_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_i32_to_u8(const int32_t* src, uint8_t* dst, int64_t n, int S, int* bad, cudaStream_t s);
 int tile_smem_bytes(int H, int L, int S, int* pitch);

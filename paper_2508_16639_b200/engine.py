@@ -419,11 +419,17 @@ class DeviceEngine:
         check(lib().escg_dev_last_timing(self._h, C.byref(ms), C.byref(n)))
         return ms.value, n.value
 
-    def draw_format(self) -> str:
-        """'wide' or 'narrow' — which attempt-word layout this engine's draws use."""
+    def draw_code(self) -> int:
+        """The draw format as the oracle names it (oracle/escg_oracle.c orc_crs_run `fmt`):
+        0 WIDE, 1 NARROW, 2 | K << 8 SLICED with K action bit planes."""
         v = C.c_int32(0)
         check(lib().escg_dev_draw_format(self._h, C.byref(v)))
-        return "narrow" if v.value else "wide"
+        return int(v.value)
+
+    def draw_format(self) -> str:
+        """'wide', 'narrow' or 'sliced' — which attempt-word layout this engine's
+        draws use."""
+        return {0: "wide", 1: "narrow", 2: "sliced"}[self.draw_code() & 0xFF]
 
     def describe(self):
         vals = [C.c_int32(0) for _ in range(4)]

@@ -124,7 +124,7 @@ def test_tile_kernel_matches_crs_oracle(escg, oracle, case):
         got3 = eng.get_lattice()
         eng.advance(4)
         got7 = eng.get_lattice()
-        narrow = eng.draw_format() == "narrow"
+        narrow = eng.draw_code()
     want3 = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 3, arity=arity, flux=flux, narrow=narrow)
     assert np.array_equal(got3, want3)
     want7 = oracle.crs_run(want3, L, H, model.matrix(), M, seed, 3, 4, arity=arity, flux=flux, narrow=narrow)
@@ -148,7 +148,7 @@ def test_block_kernel_matches_crs_oracle(escg, oracle, LH, arity, fmt, table, mo
         init = eng.get_lattice()
         eng.advance(5)
         got = eng.get_lattice()
-        narrow = eng.draw_format() == "narrow"
+        narrow = eng.draw_code()
     assert narrow == (fmt == "narrow" and L % 8 == 0)
     want = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 5, arity=arity, narrow=narrow)
     assert np.array_equal(got, want)
@@ -162,7 +162,7 @@ def test_tile_kernel_narrow_matches_crs_oracle(escg, oracle, LH, monkeypatch):
     seed = 4242
     p = params(escg, L, H, 5, 3e-3, 0.0, 4, True, seed=seed)
     with escg.DeviceEngine(p, model, kernel="tile") as eng:
-        assert eng.draw_format() == "narrow"
+        assert eng.draw_code()
         eng.init_lattice()
         init = eng.get_lattice()
         eng.advance(6)
@@ -198,7 +198,7 @@ def test_run_records_and_stop_rules(escg, oracle, kernel):
         assert st[0] == escg.RunStatus.Completed
         assert steps.tolist() == [0, 5, 10, 15, 20, 23]
         assert eng.mcs() == 23
-        narrow = eng.draw_format() == "narrow"
+        narrow = eng.draw_code()
     want = oracle.crs_run(init, L, L, model.matrix(), 1e-4, 5, 0, 23, narrow=narrow)
     assert np.array_equal(final, want)
     assert np.array_equal(counts[-1], oracle.densities(want, 3))
@@ -217,7 +217,7 @@ def test_tracked_extinction_stops_like_on_record(escg, oracle):
         steps, counts = eng.read_trace()
         t = eng.mcs()
         final = eng.get_lattice()
-        narrow = eng.draw_format() == "narrow"
+        narrow = eng.draw_code()
     assert st[0] == escg.RunStatus.Stopped
     assert counts[-1][4] == 0 and all(c[4] > 0 for c in counts[:-1])
     assert steps[-1] == t
@@ -294,7 +294,7 @@ def test_persistent_block_kernel_matches_oracle_and_launch_path(escg, oracle, LH
             st = eng.run(11, interval=3)
             steps, counts = eng.read_trace()
             outs[mode] = (a5, eng.get_lattice(), steps.tolist(), counts.tolist(), int(st[0]), eng.mcs(),
-                          eng.draw_format() == "narrow")
+                          eng.draw_code())
     assert all((np.array_equal(x, y) if isinstance(x, np.ndarray) else x == y)
                for x, y in zip(outs["1"][:6], outs["0"][:6]))
     a5, fin, steps, counts, st, m, narrow = outs["1"]
@@ -335,7 +335,7 @@ def test_band_group_equals_single_lattice(escg, oracle, n_bands, kmcs, LH):
         init = eng.get_lattice()
         eng.advance(7)
         single = eng.get_lattice()
-        narrow = eng.draw_format() == "narrow"
+        narrow = eng.draw_code()
     with BandGroup(p, model, n_bands, kmcs=kmcs) as grp:
         grp.init_lattice()
         assert np.array_equal(grp.get_lattice(), init)
@@ -496,6 +496,7 @@ def test_band_primitives_match_single_lattice(escg, n_bands, kmcs):
 
 @pytest.mark.parametrize("L,H,flux,arity,kernel,fmt", [(64, 64, True, 4, "tile", "narrow"), (48, 40, True, 8, "tile", "wide"),
                                                        (1024, 512, True, 4, "block", "narrow"),
+                                                       (1024, 512, True, 4, "block", "sliced"),
                                                        (1000, 520, True, 4, "block", "wide"),
                                                        (501, 463, True, 8, "block", "wide"),
                                                        (333, 200, False, 4, "block", "wide"),
@@ -575,3 +576,83 @@ def test_reference_simulate_dispatches_to_device_engine(escg, ref):
     assert int(got["records"]) == len(res.state.trace.counts)
     assert int(got["total"]) == L * H
     assert int(got["final_fnv"], 16) == _fnv1a_i32(res.state.lattice.cells)
+
+
+# ---- bit-sliced block kernel (draw format SLICED, csrc/slice.cu) -----------------------------------
+
+SLICED_CASES = [
+    # L, H, S, M, p0, model, forced split "nby,nbx" (None: planner), ESCG_BLOCK_MCS, expected K
+    (128, 128, 3, 1e-2, 0.1, "rps", None, None, 6),      # one group per row: the window wraps onto itself
+    (256, 64, 3, 3e-2, 0.1, "rps", "2,2", "1", 8),
+    (384, 200, 3, 1e-2, 0.0, "rps", "3,3", "2", 8),      # 3 column blocks of one group, uneven row blocks
+    (512, 96, 5, 1e-2, 0.1, "rpsls", "2,3", "4", 8),     # 3 bit planes (S = 5), 4 MCS per launch
+    (256, 256, 3, 5e-2, 0.2, "rps", "4,2", "3", 10),
+    (1024, 128, 3, 1e-1, 0.1, "rps", "1,3", "2", 12),    # column blocks of 2, 3, 3 groups
+    (1024, 256, 3, 1.0, 0.1, "rps", None, None, 16),
+]
+
+
+@pytest.mark.parametrize("case", SLICED_CASES, ids=[f"{c[0]}x{c[1]}_{c[5]}_K{c[8]}" for c in SLICED_CASES])
+def test_slice_kernel_matches_crs_oracle(escg, oracle, case, monkeypatch):
+    """The bit-sliced block kernel == oracle orc_crs_run with the SLICED draw spec, bit for bit:
+    advance in two calls (bytes -> planes -> bytes between them), then run() with records."""
+    L, H, S, M, p0, name, split, kmax, K = case
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    if split:
+        monkeypatch.setenv("ESCG_SLICE_SPLIT", split)
+    if kmax:
+        monkeypatch.setenv("ESCG_BLOCK_MCS", kmax)
+    model = model_of(escg, name)
+    seed = 0xC0FFEE + L
+    p = params(escg, L, H, S, M, p0, 4, True, seed=seed, mcs=12)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        code = eng.draw_code()
+        assert code == 2 | (K << 8), hex(code)
+        if split:
+            assert eng.describe()["ctas"] == int(split.split(",")[0]) * int(split.split(",")[1])
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(3)
+        got3 = eng.get_lattice()
+        eng.advance(4)
+        got7 = eng.get_lattice()
+        st = eng.run(12, interval=2)
+        fin = eng.get_lattice()
+        steps, counts = eng.read_trace()
+    want3 = oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 3, narrow=code)
+    assert np.array_equal(got3, want3)
+    want7 = oracle.crs_run(want3, L, H, model.matrix(), M, seed, 3, 4, narrow=code)
+    assert np.array_equal(got7, want7)
+    assert steps.tolist() == [7, 9, 11, 12] and int(st[0]) == int(escg.RunStatus.Completed)
+    cur = want7
+    for t0, t1, c in zip([7, 7, 9, 11], [7, 9, 11, 12], counts.tolist()):
+        cur = oracle.crs_run(cur, L, H, model.matrix(), M, seed, t0, t1 - t0, narrow=code) if t1 > t0 else cur
+        assert c == oracle.densities(cur, S).tolist()
+    assert np.array_equal(fin, cur)
+
+
+def test_slice_kernel_replicas_and_stops(escg, oracle, monkeypatch):
+    """Replica batches on the bit-sliced kernel: every replica equals its single run; a tracked
+    extinction stop leaves the lattice of the stopping record (plane buffer named by `cur`)."""
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    L, H, M = 256, 128, 2e-2
+    model = escg.make_circulant(3, [1])
+    seeds = [17, 18, 19]
+    p = params(escg, L, H, 3, M, 0.1, 4, True, seed=17, mcs=9)
+    with escg.DeviceEngine(p, model, n_replicas=3, seeds=seeds, kernel="block") as eng:
+        assert eng.draw_format() == "sliced"
+        eng.init_lattice()
+        inits = [eng.get_lattice(r) for r in range(3)]
+        eng.advance(5)
+        got = [eng.get_lattice(r) for r in range(3)]
+        code = eng.draw_code()
+    for r in range(3):
+        assert np.array_equal(got[r], oracle.crs_run(inits[r], L, H, model.matrix(), M, seeds[r], 0, 5, narrow=code))
+    # species 2 starts extinct: the run stops at its first record (MCS 0, before any step)
+    cells = inits[0].copy()
+    cells[cells == 2] = 1
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        eng.set_lattice(cells)
+        st = eng.run(9, interval=3, tracked=2)
+        assert int(st[0]) == int(escg.RunStatus.Stopped) and eng.mcs() == 0
+        assert np.array_equal(eng.get_lattice(), cells)
