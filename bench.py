@@ -293,9 +293,13 @@ def run_ours(args):
         traffic, tr_mcs = ncu_traffic()
         roof = {"bound": "hbm", "achieved": per_gpu * 2 / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": per_gpu * 2 / 1e9 / peak, "peak_source": peak_src,
-                "traffic": traffic, "kernel": "block_kernel (overlapped-tile CRS, %d MCS/launch)" % desc.get("kmcs", 1),
+                "traffic": traffic,
+                "kernel": ("slice_kernel (bit-sliced overlapped-tile CRS, %d MCS/launch)" if desc.get("draw_format") == "sliced"
+                           else "block_kernel (overlapped-tile CRS, %d MCS/launch)") % desc.get("kmcs", 1),
                 "algorithmic_bytes": "2 B per site-update attempt (1 B read + 1 B write of the uint8 lattice per "
-                                     "site per MCS); achieved = attempts/s x 2 B over the device-timed region",
+                                     "site per MCS); achieved = attempts/s x 2 B over the device-timed region"
+                                     + ("; during a run the lattice is held as 2-bit planes (0.5 B per attempt moved)"
+                                        if desc.get("draw_format") == "sliced" else ""),
                 "avg_launch_us": total_ms / max(launches, 1) * 1e3,
                 "traffic_per_launch_mcs": tr_mcs}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

@@ -186,6 +186,8 @@ struct escg_dev {
     int narrow = 0;  // draw format: 0 WIDE, 1 NARROW, 2 SLICED (bit-sliced block kernel)
     int K = 0;       // SLICED: action bit planes
     int npl = 2;     // SLICED: species-code bit planes
+    int lpi = 1;     // SLICED: lanes per item (slice.cu)
+    int qcap = 0;    // SLICED: deferred-tile queue capacity override (tests)
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
     int bh_max = 0, bw_max = 0;
@@ -324,8 +326,9 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
 // groups from s_i), k MCS per launch.  Work per CTA and MCS ~ (rows + 12k) x window width: the
 // bit-parallel items cover whole groups whether or not their columns are valid.
 void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
-    const int regs = (escgd::slice_kernel_registers(h->npl, h->K) + 7) / 8 * 8;
-    const int cta_per_sm = std::max(1, std::min(4, 65536 / std::max(1, regs * escgd::kSliceThreads)));
+    const int nthr = escgd::slice_threads(h->lpi);
+    const int regs = (escgd::slice_kernel_registers(h->npl, h->lpi) + 7) / 8 * 8;
+    const int cta_per_sm = std::max(1, std::min(4, 65536 / std::max(1, regs * nthr)));
     sms *= cta_per_sm;
     const int GL = h->L / 128, uy = h->H / 4;
     double best = 1e300;
@@ -338,8 +341,9 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
         for (int nbx = 1; nbx <= GL; ++nbx) {
             const int Gw = (GL + nbx - 1) / nbx + 1;
             if (Gw > 32) continue;  // a warp holds whole window rows (lanes = groups)
-            // lanes of a warp: floor(32 / Gw) tile rows x Gw groups; the rest idle through the phase
-            const double lanes = 32.0 / ((32 / Gw) * Gw);
+            // lanes of a warp: floor(32 / (lpi Gw)) tile rows x Gw groups x lpi; the rest idle
+            if ((32 / h->lpi) / Gw < 1) continue;
+            const double lanes = 32.0 / (((32 / h->lpi) / Gw) * Gw * h->lpi);
             for (int nby = 1; nby <= std::min(uy, 512); ++nby) {
                 const int bh = ((uy + nby - 1) / nby) * 4;
                 const size_t smem = static_cast<size_t>(bh + 2 * escgd::margin_rows(k)) *
@@ -360,7 +364,11 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
     }
     if (const char* sp = std::getenv("ESCG_SLICE_SPLIT")) {  // tests/experiments: "nby,nbx"
         int y = 0, x = 0;
-        if (std::sscanf(sp, "%d,%d", &y, &x) == 2 && y >= 1 && y <= uy && x >= 1 && x <= GL) {
+        if (std::sscanf(sp, "%d,%d", &y, &x) == 2 && y >= 1 && y <= uy && x >= 1 && x <= GL &&
+            (GL + x - 1) / x + 1 <= 32 &&
+            static_cast<size_t>(((uy + y - 1) / y) * 4 + 2 * escgd::margin_rows(bk)) *
+                    escgd::slice_row_words(h->npl, (GL + x - 1) / x + 1) * 4 <=
+                static_cast<size_t>(smem_cap)) {
             bnby = y;
             bnbx = x;
         }
@@ -377,7 +385,7 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
     h->smem = (bh + 2 * escgd::margin_rows(bk)) * escgd::slice_row_words(h->npl, gw) * 4;
     h->bh_max = bh;
     h->bw_max = 128 * (gw - 1);
-    h->threads = escgd::kSliceThreads;
+    h->threads = nthr;
     h->d_rows.alloc(rows.size());
     h->d_cols.alloc(cols.size());
     CK(cudaMemcpy(h->d_rows.p, rows.data(), sizeof(int) * rows.size(), cudaMemcpyHostToDevice));
@@ -481,6 +489,8 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.smem_bytes = h->smem;
     a.K = h->K;
     a.npl = h->npl;
+    a.lpi = h->lpi;
+    a.qcap = h->qcap;
     a.step = 1;
     int64_t launches = 0;
     for (int64_t done = 0; done < n;) {
@@ -632,6 +642,8 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
             a.pdst = h->pl[1].p;
             a.K = h->K;
             a.npl = h->npl;
+            a.lpi = h->lpi;
+            a.qcap = h->qcap;
             CK(escgd::launch_slice(a, h->nrep, h->stream));
             launches += 2;
         } else {
@@ -911,6 +923,11 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 h->narrow = 2;
                 h->K = std::min(lead, escgd::kSliceMaxK) & ~1;
                 h->npl = h->S <= 3 ? 2 : 3;
+                // one lane per item: measured faster than a lane pair at L=3200 (4.8e11 vs 4.3e11) and
+                // even at L=16384 (8.8e11 vs 9.0e11); the pair stays selectable (ESCG_SLICE_LPI=2)
+                h->lpi = 1;
+                if (const char* lv = std::getenv("ESCG_SLICE_LPI")) h->lpi = (h->npl == 2 && std::atoi(lv) == 2) ? 2 : 1;
+                if (const char* qv = std::getenv("ESCG_SLICE_QCAP")) h->qcap = std::atoi(qv);
             }
         }
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));

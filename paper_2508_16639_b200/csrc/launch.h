@@ -96,6 +96,8 @@ struct BlockArgs {
     uint32_t* pdst;
     int K;    // SLICED action planes
     int npl;  // bit planes (species code bits)
+    int lpi;  // lanes per bit-sliced item (1, or 2: draws and planes split over a lane pair)
+    int qcap; // > 0: deferred-tile queue capacity override (tests of the in-place overflow path)
 };
 
 // Persistent cooperative block kernel: the whole run/advance in one launch (all CTAs co-resident).
@@ -141,11 +143,17 @@ int tile_capacity(int arity, int flux, int H, int L, int threads, int smem_bytes
 int block_kernel_registers(int arity);
 cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
 // bit-sliced path (slice.cu)
-constexpr int kSliceThreads = 256;
+// CTA size of the bit-sliced kernel: 256 threads (<= 255 registers) with one lane per item, 512
+// (<= 128 registers) with a lane pair per item
+#ifndef ESCG_SLICE_T2
+#define ESCG_SLICE_T2 512
+#endif
+__host__ __device__ constexpr int slice_threads(int lpi) { return lpi == 2 ? ESCG_SLICE_T2 : 256; }
+__host__ __device__ constexpr int slice_min_blocks(int lpi) { return lpi == 2 ? 512 / ESCG_SLICE_T2 : 1; }
 constexpr int kSliceMaxK = 16;
 cudaError_t launch_slice(const BlockArgs& a, int nrep, cudaStream_t s);
 int slice_row_words(int npl, int gw);  // shared-memory words per window row (padded)
-int slice_kernel_registers(int npl, int K);
+int slice_kernel_registers(int npl, int lpi);
 // u8 lattice <-> bit planes for every replica; from_planes picks plane buffer cur[r] - 2 when cur
 // is given (replicas with cur[r] < 2 are skipped), else `buf`
 cudaError_t launch_to_planes(const uint8_t* lat, uint32_t* pl, int H, int L, int npl, int nrep, cudaStream_t s);

@@ -37,6 +37,8 @@ namespace escgd {
 namespace {
 
 constexpr uint32_t kDomSlice = 4, kDomSliceRef = 5;
+constexpr int kMaxSliceSpecies = 7;  // NPL <= 3 bit planes
+constexpr unsigned kSliceQueue = 512;  // deferred tiles per phase replayed CTA-wide
 constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint4 lds128(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
@@ -56,33 +58,34 @@ __host__ __device__ __forceinline__ int row_words(int npl, int gw) {
 }
 
 // Footprint word at column offset DX (-1..2) of a row from the group's quad words: column
-// anchor + DX = 4b + t with t = XR + DX, i.e. quad t & 3 at bit b + (t >> 2).
-template <int XR, int DX>
+// anchor + DX = 4b + t with t = XR + DX, i.e. quad t & 3 at bit b + (t >> 2).  The neighbouring
+// groups' copies sit D lanes away (D = lanes per item).
+template <int XR, int DX, int D>
 __device__ __forceinline__ uint32_t fetch(const uint32_t (&q4)[4]) {
     constexpr int t = XR + DX, q = t & 3, s = t < 0 ? -1 : (t >> 2);
     if constexpr (s == 0) {
         return q4[q];
     } else if constexpr (s < 0) {  // bit b-1: this group's quad 3 shifted up, bit 0 from the left group
-        const uint32_t l = __shfl_up_sync(kFull, q4[3], 1);
+        const uint32_t l = __shfl_up_sync(kFull, q4[3], D);
         return __funnelshift_l(l, q4[3], 1);
     } else {  // bit b+1: shifted down, bit 31 from the right group
-        const uint32_t r = __shfl_down_sync(kFull, q4[q], 1);
+        const uint32_t r = __shfl_down_sync(kFull, q4[q], D);
         return __funnelshift_r(q4[q], r, 1);
     }
 }
 
 // Inverse of fetch: write the footprint word back into the group's quad word (the bit that belongs
 // to the neighbouring group is taken over by that group's lane from its own copy).
-template <int XR, int DX>
+template <int XR, int DX, int D>
 __device__ __forceinline__ void put(uint32_t (&q4)[4], uint32_t f) {
     constexpr int t = XR + DX, q = t & 3, s = t < 0 ? -1 : (t >> 2);
     if constexpr (s == 0) {
         q4[q] = f;
     } else if constexpr (s < 0) {
-        const uint32_t r = __shfl_down_sync(kFull, f, 1);
+        const uint32_t r = __shfl_down_sync(kFull, f, D);
         q4[3] = __funnelshift_r(f, r, 1);
     } else {
-        const uint32_t l = __shfl_up_sync(kFull, f, 1);
+        const uint32_t l = __shfl_up_sync(kFull, f, D);
         q4[q] = __funnelshift_l(l, f, 1);
     }
 }
@@ -97,8 +100,11 @@ struct SliceCtx {
     bool bigy;         // window taller than the lattice (true modulo)
     uint32_t s32;
     uint32_t xm, xi, TK;  // X_mig, X_int, the undecided action prefix (K leading ones)
-    const uint32_t* T;    // exact interaction thresholds (global)
+    uint32_t sT;          // exact interaction thresholds (shared-memory address, (S+1)^2 words)
     int S1;
+    uint4* q;             // deferred-tile queue of the phase: (w | acol << 16, code, item)
+    unsigned* qn;         // its fill count
+    unsigned qcap;        // its capacity (<= kSliceQueue; smaller in tests of the overflow path)
 };
 
 // Exact replay of one tile whose attempts left the bit-parallel pass (engine.hpp:108-141 on
@@ -107,7 +113,7 @@ struct SliceCtx {
 template <int NPL>
 __device__ __noinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code, uint32_t item,
                                           int l, uint32_t c1, uint32_t c2r, uint32_t s32, uint32_t xm, uint32_t xi,
-                                          uint32_t TK, const uint32_t* T, int S1) {
+                                          uint32_t TK, uint32_t sT, int S1) {
     const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);
     const int Wc = 128 * Gw;
     const uint32_t PS = static_cast<uint32_t>(Gw) * 16u;  // plane stride (bytes)
@@ -132,7 +138,7 @@ __device__ __noinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, i
         if (s == n || s >= static_cast<uint32_t>(S1) || n >= static_cast<uint32_t>(S1)) continue;
         uint32_t ns = n, nn = s;  // certain migration
         if ((code >> (16 + a)) & 1u) {
-            const uint32_t r = rule_exact(s, n, TK | (rw & ~TK), xm, xi, T, S1);
+            const uint32_t r = rule_exact_s(s, n, TK | (rw & ~TK), xm, xi, sT, S1);
             ns = r & 0xFFu;
             nn = r >> 8;
         }
@@ -147,11 +153,16 @@ __device__ __noinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, i
 }
 
 // One colour phase: tile rows i_lo .. i_lo + nrows - 1 (anchor window row 4i + yr), every window
-// group, anchor column residue XR.
-template <int NPL, int K, int XR>
+// group, anchor column residue XR.  LPI lanes per item: with 2 (NPL = 2) the pair splits the draws
+// (attempts {0,1} / {2,3}: two choice draws and K/2 action draws each, exchanged by shuffles) and the
+// planes (lane h updates plane h), so a phase has twice the warps with half the latency each.
+template <int NPL, int K, int XR, int LPI>
 __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, int i_lo, int nrows, uint32_t c1,
                                             uint32_t c2s, uint32_t c2r) {
-    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    static_assert(LPI == 1 || (LPI == 2 && NPL == 2 && K % 2 == 0), "lane split: two planes, even K");
+    constexpr int NP = NPL / LPI;  // planes per lane
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = threadIdx.x & 31;
+    const int h = LPI == 2 ? (lane & 1) : 0, pbase = lane & ~(LPI - 1);
     const int Hh = C.Hg >> 1;
 #pragma unroll 1
     for (int base = warp * C.RW; base < nrows; base += nwarps * C.RW) {  // uniform per warp
@@ -166,35 +177,61 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         g = g >= C.GL ? g - C.GL : g;
         const uint32_t item = static_cast<uint32_t>(j) * static_cast<uint32_t>(C.GL) + static_cast<uint32_t>(g);
 
-        // action planes (draws 4 .. 4+K-1): undecided = all K leading bits one
-        uint32_t U[4] = {~0u, ~0u, ~0u, ~0u};
+        // action planes (draws 4 .. 4+K-1, attempt a = word / K): undecided = all K leading bits one
+        // choice planes (draws 0..3): cell row, cell column, direction bits
+        uint32_t U[4], Y[4], X[4], D0[4], D1[4];
+        if constexpr (LPI == 1) {
 #pragma unroll
-        for (int jj = 0; jj < K; ++jj) {
-            const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(4 + jj) << 24), C.s32);
-            const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+            for (int a = 0; a < 4; ++a) U[a] = ~0u;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) U[(4 * jj + c) / K] &= vw[c];
+            for (int jj = 0; jj < K; ++jj) {
+                const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(4 + jj) << 24), C.s32);
+                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) U[(4 * jj + c) / K] &= vw[c];
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(a) << 24), C.s32);
+                Y[a] = v.x;
+                X[a] = v.y;
+                D0[a] = v.z;
+                D1[a] = v.w;
+            }
+        } else {
+            // lane h: attempts 2h, 2h+1 (action words [2hK, 2hK + 2K) = draws 4 + hK/2 .. 4 + hK/2 + K/2 - 1)
+            uint32_t Ul[2] = {~0u, ~0u};
+#pragma unroll
+            for (int t = 0; t < K / 2; ++t) {
+                const uint32_t jj = 4u + static_cast<uint32_t>(h * (K / 2) + t);
+                const uint4 v = philox(item, c1, c2s | (jj << 24), C.s32);
+                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) Ul[(4 * t + c) / K] &= vw[c];
+            }
+            const uint4 v0 = philox(item, c1, c2s | (static_cast<uint32_t>(2 * h) << 24), C.s32);
+            const uint4 v1 = philox(item, c1, c2s | (static_cast<uint32_t>(2 * h + 1) << 24), C.s32);
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int src = pbase + (a >> 1);
+                const uint4 v = (a & 1) ? v1 : v0;
+                U[a] = __shfl_sync(kFull, Ul[a & 1], src);
+                Y[a] = __shfl_sync(kFull, v.x, src);
+                X[a] = __shfl_sync(kFull, v.y, src);
+                D0[a] = __shfl_sync(kFull, v.z, src);
+                D1[a] = __shfl_sync(kFull, v.w, src);
+            }
         }
         const uint32_t Dm = valid ? (U[0] | U[1] | U[2] | U[3]) : 0u;
         const uint32_t act = ~Dm;
-        // choice planes (draws 0..3): cell row, cell column, direction bits
-        uint32_t Y[4], X[4], D0[4], D1[4];
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(a) << 24), C.s32);
-            Y[a] = v.x;
-            X[a] = v.y;
-            D0[a] = v.z;
-            D1[a] = v.w;
-        }
 
-        // footprint rows w-1 .. w+2 of this group (all planes)
-        uint32_t Q[4][NPL][4];
-        uint32_t* rowp = C.sw + (valid ? w - 1 : 0) * C.RP + C.gw * 4;
+        // footprint rows w-1 .. w+2 of this group (this lane's planes)
+        uint32_t Q[4][NP][4];
+        uint32_t* rowp = C.sw + (valid ? w - 1 : 0) * C.RP + C.gw * 4 + h * NP * C.Gw * 4;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
 #pragma unroll
-            for (int p = 0; p < NPL; ++p) {
+            for (int p = 0; p < NP; ++p) {
                 uint4 t = make_uint4(0u, 0u, 0u, 0u);
                 if (valid) t = lds128(rowp + rr * C.RP + p * C.Gw * 4);
                 Q[rr][p][0] = t.x;
@@ -203,9 +240,9 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
                 Q[rr][p][3] = t.w;
             }
         }
-        uint32_t F[4][4][NPL];  // [row][column offset + 1][plane]; corners unused
+        uint32_t F[4][4][NP];  // [row][column offset + 1][plane]; corners unused
 #define ESCG_FET(rr, c)                                                         \
-    _Pragma("unroll") for (int p = 0; p < NPL; ++p) F[rr][c][p] = fetch<XR, (c)-1>(Q[rr][p]);
+    _Pragma("unroll") for (int p = 0; p < NP; ++p) F[rr][c][p] = fetch<XR, (c)-1, LPI>(Q[rr][p]);
         ESCG_FET(0, 1) ESCG_FET(0, 2)
         ESCG_FET(1, 0) ESCG_FET(1, 1) ESCG_FET(1, 2) ESCG_FET(1, 3)
         ESCG_FET(2, 0) ESCG_FET(2, 1) ESCG_FET(2, 2) ESCG_FET(2, 3)
@@ -225,7 +262,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
             const uint32_t mV2[2] = {y & nx & dn, y & x & dn};
             const uint32_t mH[2][3] = {{ny & nx & lf, ny & hm, ny & x & rt}, {y & nx & lf, y & hm, y & x & rt}};
 #pragma unroll
-            for (int p = 0; p < NPL; ++p) {
+            for (int p = 0; p < NP; ++p) {
                 uint32_t dV0[2], dV1[2], dV2[2], dH[2][3];
 #pragma unroll
                 for (int xx = 0; xx < 2; ++xx) {
@@ -252,7 +289,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         }
 
 #define ESCG_PUT(rr, c) \
-    _Pragma("unroll") for (int p = 0; p < NPL; ++p) put<XR, (c)-1>(Q[rr][p], F[rr][c][p]);
+    _Pragma("unroll") for (int p = 0; p < NP; ++p) put<XR, (c)-1, LPI>(Q[rr][p], F[rr][c][p]);
         ESCG_PUT(0, 1) ESCG_PUT(0, 2)
         ESCG_PUT(1, 0) ESCG_PUT(1, 1) ESCG_PUT(1, 2) ESCG_PUT(1, 3)
         ESCG_PUT(2, 0) ESCG_PUT(2, 1) ESCG_PUT(2, 2) ESCG_PUT(2, 3)
@@ -262,12 +299,13 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr)
 #pragma unroll
-                for (int p = 0; p < NPL; ++p)
+                for (int p = 0; p < NP; ++p)
                     sts128(rowp + rr * C.RP + p * C.Gw * 4, make_uint4(Q[rr][p][0], Q[rr][p][1], Q[rr][p][2], Q[rr][p][3]));
         }
         __syncwarp();
-        // deferred tiles: exact replay by their lane (rare: ~4 per warp-item at P(migration) = 0.999)
-        for (uint32_t dm = Dm; dm != 0u; dm &= dm - 1u) {
+        // deferred tiles (rare: ~4 per 1024 tiles at P(migration) 0.999): queued for the phase's
+        // replay pass, which spreads them over the CTA (one thread each) after the bulk barrier
+        for (uint32_t dm = h == 0 ? Dm : 0u; dm != 0u; dm &= dm - 1u) {
             const int l = __ffs(dm) - 1;
             uint32_t code = 0;
 #pragma unroll
@@ -277,19 +315,38 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
                         << (4 * a);
                 code |= ((U[a] >> l) & 1u) << (16 + a);
             }
-            slice_replay<NPL>(C.sw0, C.RP, C.Gw, w, 128 * C.gw + 4 * l + XR, code, item, l, c1, c2r, C.s32, C.xm,
-                              C.xi, C.TK, C.T, C.S1);
+            const int acol = 128 * C.gw + 4 * l + XR;
+            const unsigned slot = atomicAdd(C.qn, 1u);
+            if (slot < C.qcap) {
+                C.q[slot] = make_uint4(static_cast<uint32_t>(w) | (static_cast<uint32_t>(acol) << 16), code, item, 0u);
+            } else {  // queue full: replay in place (the tile's footprint is disjoint from every other)
+                slice_replay<NPL>(C.sw0, C.RP, C.Gw, w, acol, code, item, l, c1, c2r, C.s32, C.xm, C.xi, C.TK, C.sT,
+                                  C.S1);
+            }
         }
-        __syncwarp();
     }
 }
 
-#ifndef ESCG_SLICE_MINB
-#define ESCG_SLICE_MINB 1
-#endif
-template <int NPL, int K>
-__global__ void __launch_bounds__(kSliceThreads, ESCG_SLICE_MINB) slice_kernel(BlockArgs a) {
+// The phase's replay pass: queued deferred tiles, one per thread (after the bulk barrier), dealt
+// round-robin over the warps so that each warp runs few (divergent) replays side by side.
+template <int NPL>
+__device__ __forceinline__ void slice_replay_queue(const SliceCtx& C, unsigned n, uint32_t c1, uint32_t c2r) {
+    n = n < C.qcap ? n : C.qcap;
+    const unsigned nw = blockDim.x >> 5;
+    for (unsigned i = (threadIdx.x & 31) * nw + (threadIdx.x >> 5); i < n; i += blockDim.x) {
+        const uint4 e = C.q[i];
+        const int w = static_cast<int>(e.x & 0xFFFFu), acol = static_cast<int>(e.x >> 16);
+        slice_replay<NPL>(C.sw0, C.RP, C.Gw, w, acol, e.y, e.z, (acol >> 2) & 31, c1, c2r, C.s32, C.xm, C.xi, C.TK,
+                          C.sT, C.S1);
+    }
+}
+
+template <int NPL, int K, int LPI>
+__global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) slice_kernel(BlockArgs a) {
     extern __shared__ __align__(16) uint32_t sw[];
+    __shared__ uint32_t sTh[(kMaxSliceSpecies + 1) * (kMaxSliceSpecies + 1)];
+    __shared__ uint4 sQ[kSliceQueue];
+    __shared__ unsigned sQn[3];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int r = blockIdx.z, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const int Hg = a.H, GL = a.L >> 7, S1 = a.S + 1;
@@ -306,6 +363,8 @@ __global__ void __launch_bounds__(kSliceThreads, ESCG_SLICE_MINB) slice_kernel(B
     __shared__ uint32_t sCnt[1 << NPL];
     __shared__ int sLast;
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
+    if (tid < 3) sQn[tid] = 0u;
+    for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
 
@@ -327,9 +386,9 @@ __global__ void __launch_bounds__(kSliceThreads, ESCG_SLICE_MINB) slice_kernel(B
         C.sw0 = smem_addr(sw);
         C.RP = RP;
         C.Gw = Gw;
-        C.RW = 32 / Gw;
-        C.tr = lane / Gw;
-        C.gw = lane - C.tr * Gw;
+        C.RW = (32 / LPI) / Gw;
+        C.tr = (lane / LPI) / Gw;
+        C.gw = lane / LPI - C.tr * Gw;
         C.gs0 = gs0;
         C.GL = GL;
         C.Hg = Hg;
@@ -339,7 +398,9 @@ __global__ void __launch_bounds__(kSliceThreads, ESCG_SLICE_MINB) slice_kernel(B
         C.xm = a.rule.xm;
         C.xi = a.rule.xi;
         C.TK = ~0u << (32 - K);
-        C.T = a.rule.T;
+        C.sT = smem_addr(sTh);
+        C.q = sQ;
+        C.qcap = a.qcap > 0 && a.qcap < static_cast<int>(kSliceQueue) ? static_cast<unsigned>(a.qcap) : kSliceQueue;
         C.S1 = S1;
 #pragma unroll 1
         for (int t = 0; t < a.nmcs; ++t) {
@@ -358,13 +419,22 @@ __global__ void __launch_bounds__(kSliceThreads, ESCG_SLICE_MINB) slice_kernel(B
                 const uint32_t c1 = static_cast<uint32_t>(mcs);
                 const uint32_t c2s = ctr2(mcs, kDomSlice, static_cast<uint32_t>(p), 0u);
                 const uint32_t c2r = ctr2(mcs, kDomSliceRef, static_cast<uint32_t>(p), 0u);
+                // queue counters rotate over three phases: the next phase's counter was last read
+                // before this phase's predecessor's barrier, so it can be zeroed now
+                C.qn = &sQn[q % 3];
+                if (tid == 0) sQn[(q + 1) % 3] = 0u;
                 switch (xr) {
-                    case 0: slice_phase<NPL, K, 0>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
-                    case 1: slice_phase<NPL, K, 1>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
-                    case 2: slice_phase<NPL, K, 2>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
-                    default: slice_phase<NPL, K, 3>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
+                    case 0: slice_phase<NPL, K, 0, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
+                    case 1: slice_phase<NPL, K, 1, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
+                    case 2: slice_phase<NPL, K, 2, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
+                    default: slice_phase<NPL, K, 3, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
                 }
                 __syncthreads();
+                const unsigned nq = sQn[q % 3];
+                if (nq != 0u) {  // uniform
+                    slice_replay_queue<NPL>(C, nq, c1, c2r);
+                    __syncthreads();
+                }
             }
         }
         // block region: rows [My, My + bh), columns [64, 128 Gw - 64): the edge groups own one half
@@ -498,9 +568,9 @@ int conv_grid(int64_t units) {
     return g < 1 ? 1 : static_cast<int>(g);
 }
 
-template <int NPL, int K>
+template <int NPL, int K, int LPI>
 cudaError_t slice_launch_t(const BlockArgs& a, int nrep, cudaStream_t s) {
-    auto k = slice_kernel<NPL, K>;
+    auto k = slice_kernel<NPL, K, LPI>;
     static std::atomic<int> configured[kMaxDevices];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -517,7 +587,7 @@ cudaError_t slice_launch_t(const BlockArgs& a, int nrep, cudaStream_t s) {
     static const bool pdl = !(std::getenv("ESCG_PDL") && std::getenv("ESCG_PDL")[0] == '0');
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(static_cast<unsigned>(a.nbx), static_cast<unsigned>(a.nby), static_cast<unsigned>(nrep));
-    cfg.blockDim = dim3(kSliceThreads);
+    cfg.blockDim = dim3(static_cast<unsigned>(slice_threads(LPI)));
     cfg.dynamicSmemBytes = static_cast<size_t>(a.smem_bytes);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -528,15 +598,15 @@ cudaError_t slice_launch_t(const BlockArgs& a, int nrep, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k, a);
 }
 
-template <int NPL>
+template <int NPL, int LPI>
 cudaError_t slice_launch_npl(const BlockArgs& a, int nrep, cudaStream_t s) {
     switch (a.K) {
-        case 6: return slice_launch_t<NPL, 6>(a, nrep, s);
-        case 8: return slice_launch_t<NPL, 8>(a, nrep, s);
-        case 10: return slice_launch_t<NPL, 10>(a, nrep, s);
-        case 12: return slice_launch_t<NPL, 12>(a, nrep, s);
-        case 14: return slice_launch_t<NPL, 14>(a, nrep, s);
-        case 16: return slice_launch_t<NPL, 16>(a, nrep, s);
+        case 6: return slice_launch_t<NPL, 6, LPI>(a, nrep, s);
+        case 8: return slice_launch_t<NPL, 8, LPI>(a, nrep, s);
+        case 10: return slice_launch_t<NPL, 10, LPI>(a, nrep, s);
+        case 12: return slice_launch_t<NPL, 12, LPI>(a, nrep, s);
+        case 14: return slice_launch_t<NPL, 14, LPI>(a, nrep, s);
+        case 16: return slice_launch_t<NPL, 16, LPI>(a, nrep, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -546,16 +616,17 @@ cudaError_t slice_launch_npl(const BlockArgs& a, int nrep, cudaStream_t s) {
 int slice_row_words(int npl, int gw) { return row_words(npl, gw); }
 
 cudaError_t launch_slice(const BlockArgs& a, int nrep, cudaStream_t s) {
-    if (a.npl == 2) return slice_launch_npl<2>(a, nrep, s);
-    if (a.npl == 3) return slice_launch_npl<3>(a, nrep, s);
+    if (a.npl == 2 && a.lpi == 2) return slice_launch_npl<2, 2>(a, nrep, s);
+    if (a.npl == 2) return slice_launch_npl<2, 1>(a, nrep, s);
+    if (a.npl == 3) return slice_launch_npl<3, 1>(a, nrep, s);
     return cudaErrorInvalidValue;
 }
 
-int slice_kernel_registers(int npl, int K) {
+int slice_kernel_registers(int npl, int lpi) {
     cudaFuncAttributes fa{};
-    const void* f = npl == 3 ? reinterpret_cast<const void*>(slice_kernel<3, 10>)
-                             : reinterpret_cast<const void*>(slice_kernel<2, 10>);
-    (void)K;
+    const void* f = npl == 3   ? reinterpret_cast<const void*>(slice_kernel<3, 10, 1>)
+                    : lpi == 2 ? reinterpret_cast<const void*>(slice_kernel<2, 10, 2>)
+                               : reinterpret_cast<const void*>(slice_kernel<2, 10, 1>);
     if (cudaFuncGetAttributes(&fa, f) != cudaSuccess) return 255;
     return fa.numRegs;
 }

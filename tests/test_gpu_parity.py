@@ -592,12 +592,17 @@ SLICED_CASES = [
 ]
 
 
+@pytest.mark.parametrize("lpi,qcap", [("1", None), ("2", None), ("2", "3")])
 @pytest.mark.parametrize("case", SLICED_CASES, ids=[f"{c[0]}x{c[1]}_{c[5]}_K{c[8]}" for c in SLICED_CASES])
-def test_slice_kernel_matches_crs_oracle(escg, oracle, case, monkeypatch):
+def test_slice_kernel_matches_crs_oracle(escg, oracle, case, lpi, qcap, monkeypatch):
     """The bit-sliced block kernel == oracle orc_crs_run with the SLICED draw spec, bit for bit:
-    advance in two calls (bytes -> planes -> bytes between them), then run() with records."""
+    advance in two calls (bytes -> planes -> bytes between them), then run() with records.  One
+    and two lanes per item; a 3-entry deferred-tile queue forces the in-place overflow path."""
     L, H, S, M, p0, name, split, kmax, K = case
     monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    monkeypatch.setenv("ESCG_SLICE_LPI", lpi)
+    if qcap:
+        monkeypatch.setenv("ESCG_SLICE_QCAP", qcap)
     if split:
         monkeypatch.setenv("ESCG_SLICE_SPLIT", split)
     if kmax:

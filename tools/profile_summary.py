@@ -1,6 +1,6 @@
 """Summarise a gpurun ncu launch list + one --set full capture into profiles/ (committed evidence).
 
-    python tools/profile_summary.py <round-tag> gpurun_out/launches.csv gpurun_out/prof.ncu-rep
+    python tools/profile_summary.py <round-tag> gpurun_out/launches.csv gpurun_out/prof.ncu-rep <mcs/launch> [kernel] [capture command]
 """
 import collections
 import csv
@@ -32,6 +32,10 @@ def ncu_raw(rep):
     return [dict(zip(hdr, v)) for v in rows[2:]]
 
 
+KERNEL = sys.argv[5] if len(sys.argv) > 5 else "block_kernel"
+CAPTURE = sys.argv[6] if len(sys.argv) > 6 else "`python tools/one_block.py 3200 200` (ncu --set full -s 50 -c 1)"
+
+
 def main():
     tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
     prof = os.path.join(ROOT, "profiles")
@@ -41,8 +45,8 @@ def main():
     lines = ["# %s launch list (ncu --metrics gpu__time_duration.sum --clock-control none)" % tag, "",
              "Command: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline` (first 700 launches).",
              "Per-launch times are cold-cache and serialised (compare shares, not absolutes).",
-             "Full capture (`*_block_kernel_ncu_details.txt`, `ncu_summary.json`): one steady-state 2-MCS launch of "
-             "`python tools/one_block.py 3200 200` (ncu --set full -s 50 -c 1), the bench's block kernel shape.", "",
+             "Full capture (`%s_%s_ncu_details.txt`, `ncu_summary.json`): one steady-state launch of %s, the bench's "
+             "kernel shape." % (tag, KERNEL, CAPTURE), "",
              "| kernel | launches | mean us | total us | share |", "|---|---|---|---|---|"]
     for k, v in agg.items():
         lines.append("| %s | %d | %.2f | %.1f | %.1f%% |" % (k, len(v), sum(v) / len(v), sum(v), 100 * sum(v) / tot))
@@ -63,7 +67,7 @@ def main():
         units = dict(zip(rows[0], rows[1]))
     except Exception:
         pass
-    summ = {"tag": tag, "captures": [{k: c.get(k) for k in keys} for c in caps], "units": {k: units.get(k) for k in keys}}
+    summ = {"tag": tag, "kernel": KERNEL, "capture": CAPTURE, "captures": [{k: c.get(k) for k in keys} for c in caps], "units": {k: units.get(k) for k in keys}}
     # DRAM bytes per launch of the dominant kernel (the full-MCS-count launch = largest duration)
     big = max(caps, key=lambda c: float(c["gpu__time_duration.sum"]))
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -74,7 +78,7 @@ def main():
     summ["warp_inst_per_launch"] = float(big["smsp__inst_executed.sum"])
     json.dump(summ, open(os.path.join(prof, "ncu_summary.json"), "w"), indent=1)
     det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
-    open(os.path.join(prof, "%s_block_kernel_ncu_details.txt" % tag), "w").write(det)
+    open(os.path.join(prof, "%s_%s_ncu_details.txt" % (tag, KERNEL)), "w").write(det)
     print("\n".join(lines))
     print(json.dumps(summ["captures"], indent=1)[:2000])
 

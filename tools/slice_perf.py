@@ -28,10 +28,15 @@ def probe(L, n_mcs, fmt, M=1e-4, p0=0.1):
 if __name__ == "__main__":
     fmts = ("narrow", "sliced")
     args = sys.argv[1:]
-    if args and args[0].startswith("--fmt="):
-        fmts = (args.pop(0)[6:],)
+    M = 1e-4
+    while args and args[0].startswith("--"):
+        a = args.pop(0)
+        if a.startswith("--fmt="):
+            fmts = (a[6:],)
+        elif a.startswith("--M="):
+            M = float(a[4:])
     Ls = [int(a) for a in args] or [3200, 16384]
     for L in Ls:
         n = 400 if L <= 4096 else 20
         for fmt in fmts:
-            print(json.dumps(probe(L, n, fmt)), flush=True)
+            print(json.dumps(dict(probe(L, n, fmt, M=M), M=M)), flush=True)
