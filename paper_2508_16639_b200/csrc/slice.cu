@@ -36,6 +36,18 @@
 namespace escgd {
 namespace {
 
+#ifdef ESCG_DIAG_SLICE
+// diagnostic builds only (tools/slice_diag.py): clock64 stamps of CTA 0..3, warps 0..15, phases 0..7
+__device__ long long g_sdiag[4][16][8][8];
+#define SDIAG(ph, ev)                                                                                  \
+    do {                                                                                              \
+        const int cta_ = blockIdx.x + gridDim.x * blockIdx.y;                                         \
+        if (cta_ < 4 && (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 16 && (ph) < 8)                \
+            g_sdiag[cta_][threadIdx.x >> 5][ph][ev] = clock64();                                      \
+    } while (0)
+#else
+#define SDIAG(ph, ev)
+#endif
 constexpr uint32_t kDomSlice = 4, kDomSliceRef = 5;
 constexpr int kMaxSliceSpecies = 7;  // NPL <= 3 bit planes
 constexpr unsigned kSliceQueue = 512;  // deferred tiles per phase replayed CTA-wide
@@ -107,49 +119,86 @@ struct SliceCtx {
     unsigned qcap;        // its capacity (<= kSliceQueue; smaller in tests of the overflow path)
 };
 
-// Exact replay of one tile whose attempts left the bit-parallel pass (engine.hpp:108-141 on
-// shared-memory bits; sw0 = shared address of the window).  code: 4 choice bits per attempt (cell
-// row, cell column, direction) in nibble a, undecided flag of attempt a in bit 16 + a.
+// Exact replay of one tile whose attempts left the bit-parallel pass (engine.hpp:108-141), on the
+// tile's 12 footprint cells held as 3-bit fields of one register: the cells are read once, the four
+// attempts run branch-free in registers, and the changed bits are written back with shared-memory
+// XOR reductions (neighbouring lanes share the boundary words).  sw0 = shared address of the
+// window; code: 4 choice bits per attempt (cell row, cell column, direction) in nibble a,
+// undecided flag of attempt a in bit 16 + a.  Footprint positions: 0 (0,1) 1 (0,2) 2 (1,0) 3 (1,1)
+// 4 (1,2) 5 (1,3) 6 (2,0) 7 (2,1) 8 (2,2) 9 (2,3) 10 (3,1) 11 (3,2) as (row - w + 1, col - acol + 1).
 template <int NPL>
-__device__ __noinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code, uint32_t item,
-                                          int l, uint32_t c1, uint32_t c2r, uint32_t s32, uint32_t xm, uint32_t xi,
-                                          uint32_t TK, uint32_t sT, int S1) {
+__device__ __forceinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code,
+                                             uint32_t item, int l, uint32_t c1, uint32_t c2r, uint32_t s32, uint32_t xm,
+                                             uint32_t xi, uint32_t TK, uint32_t sT, int S1, int qd = 8) {
+    constexpr int kRow[12] = {0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3};
+    constexpr int kCol[12] = {1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 1, 2};
+    constexpr uint32_t kCellPos = 0x8473u;               // position of cell (Y, X): nibble Y | X << 1
+    constexpr uint64_t kNbrPos = 0x95847362b8a74130ull;  // neighbour position: nibble Y | X << 1 | dir << 2
+    if (acol < 1 || acol + 2 >= 128 * Gw) return;  // window edge: margin cells, never stored
+#ifdef ESCG_DIAG_REPLAY_NOPHILOX
+    const uint4 rf = make_uint4(item ^ c1, c2r + l, s32, item);
+#else
     const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);
-    const int Wc = 128 * Gw;
+#endif
     const uint32_t PS = static_cast<uint32_t>(Gw) * 16u;  // plane stride (bytes)
+    uint32_t addr[12], bit[12];
+    uint64_t cells = 0;
+#pragma unroll
+    for (int k = 0; k < 12; ++k) {
+        const int row = w - 1 + kRow[k], col = acol - 1 + kCol[k];
+        addr[k] = sw0 + 4u * static_cast<uint32_t>(row * RP + (col >> 7) * 4 + (col & 3));
+        bit[k] = (static_cast<uint32_t>(col) >> 2) & 31u;
+        uint32_t v = 0;
+#pragma unroll
+        for (int p = 0; p < NPL; ++p) v |= ((lds32o(addr[k] + p * PS) >> bit[k]) & 1u) << p;
+        cells |= static_cast<uint64_t>(v) << (3 * k);
+    }
+#ifdef ESCG_DIAG_SLICE
+    if ((cells + rf.x) != 1u) SDIAG(qd, 6);
+#endif
+    const uint64_t cells0 = cells;
+    const uint32_t rw[4] = {rf.x, rf.y, rf.z, rf.w};
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
-        const uint32_t rw = a == 0 ? rf.x : (a == 1 ? rf.y : (a == 2 ? rf.z : rf.w));
         const uint32_t cb = (code >> (4 * a)) & 15u;
-        const int sr = w + static_cast<int>(cb & 1u), sc = acol + static_cast<int>((cb >> 1) & 1u);
-        const uint32_t dir = (cb >> 2) & 3u;
-        const int nr = sr + (dir == 0u ? -1 : (dir == 1u ? 1 : 0));
-        const int nc = sc + (dir == 2u ? -1 : (dir == 3u ? 1 : 0));
-        if (nc < 0 || nc >= Wc || sc >= Wc) return;  // window edge: margin cells, never stored
-        const uint32_t sa = sw0 + 4u * static_cast<uint32_t>(sr * RP + (sc >> 7) * 4 + (sc & 3));
-        const uint32_t na = sw0 + 4u * static_cast<uint32_t>(nr * RP + (nc >> 7) * 4 + (nc & 3));
-        const uint32_t sb = (static_cast<uint32_t>(sc) >> 2) & 31u, nb = (static_cast<uint32_t>(nc) >> 2) & 31u;
-        uint32_t s = 0, n = 0;
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) {
-            s |= ((lds32o(sa + p * PS) >> sb) & 1u) << p;
-            n |= ((lds32o(na + p * PS) >> nb) & 1u) << p;
-        }
-        if (s == n || s >= static_cast<uint32_t>(S1) || n >= static_cast<uint32_t>(S1)) continue;
-        uint32_t ns = n, nn = s;  // certain migration
-        if ((code >> (16 + a)) & 1u) {
-            const uint32_t r = rule_exact_s(s, n, TK | (rw & ~TK), xm, xi, sT, S1);
-            ns = r & 0xFFu;
-            nn = r >> 8;
-        }
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) {
-            if (((s ^ ns) >> p) & 1u)
-                asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(sa + p * PS), "r"(1u << sb) : "memory");
-            if (((n ^ nn) >> p) & 1u)
-                asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(na + p * PS), "r"(1u << nb) : "memory");
-        }
+        const uint32_t ps = (kCellPos >> (4 * (cb & 3u))) & 15u, pn = static_cast<uint32_t>(kNbrPos >> (4 * cb)) & 15u;
+        const uint32_t s = static_cast<uint32_t>(cells >> (3 * ps)) & 7u, n = static_cast<uint32_t>(cells >> (3 * pn)) & 7u;
+        // the rule (engine.hpp:111-140) with selects; a decided attempt is a certain migration
+        const bool und = (code >> (16 + a)) & 1u;
+        const uint32_t x = TK | (rw[a] & ~TK);
+        const bool mig = !und || x < xm, rep = und && x >= xi;
+        const bool inter = !mig && !rep && s != 0u && n != 0u && s != n;
+        const uint32_t t1 = lds32_if(inter, sT + 4u * (s * S1 + n), 0u);
+        const uint32_t t2 = lds32_if(inter, sT + 4u * (n * S1 + s), 0u);
+        const bool kn = inter && x < t1, ks = inter && !(x < t1) && x < t2;
+        const bool r1 = rep && n == 0u, r2 = rep && n != 0u && s == 0u;
+        const uint32_t ns = mig ? n : (ks ? 0u : (r2 ? n : s));
+        const uint32_t nn = mig ? s : (kn ? 0u : (r1 ? s : n));
+        cells = (cells & ~((7ull << (3 * ps)) | (7ull << (3 * pn)))) | (static_cast<uint64_t>(ns) << (3 * ps)) |
+                (static_cast<uint64_t>(nn) << (3 * pn));
     }
+    const uint64_t delta = cells ^ cells0;
+#ifdef ESCG_DIAG_SLICE
+    if (delta != 1u) SDIAG(qd, 5);
+#endif
+#ifndef ESCG_DIAG_REPLAY_NOATOM
+#pragma unroll
+    for (int k = 0; k < 12; ++k)
+#pragma unroll
+        for (int p = 0; p < NPL; ++p)
+            if ((delta >> (3 * k + p)) & 1u)
+                asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[k] + p * PS), "r"(1u << bit[k]) : "memory");
+#else
+    if (delta == 0x123456789ull) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[0]), "r"(1u) : "memory");
+#endif
+}
+
+// Out-of-line copy for the in-place overflow path inside the (per-residue) phase bodies.
+template <int NPL>
+__device__ __noinline__ void slice_replay_ool(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code,
+                                              uint32_t item, int l, uint32_t c1, uint32_t c2r, uint32_t s32,
+                                              uint32_t xm, uint32_t xi, uint32_t TK, uint32_t sT, int S1) {
+    slice_replay<NPL>(sw0, RP, Gw, w, acol, code, item, l, c1, c2r, s32, xm, xi, TK, sT, S1);
 }
 
 // One colour phase: tile rows i_lo .. i_lo + nrows - 1 (anchor window row 4i + yr), every window
@@ -158,7 +207,7 @@ __device__ __noinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, i
 // planes (lane h updates plane h), so a phase has twice the warps with half the latency each.
 template <int NPL, int K, int XR, int LPI>
 __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, int i_lo, int nrows, uint32_t c1,
-                                            uint32_t c2s, uint32_t c2r) {
+                                            uint32_t c2s, uint32_t c2r, int qd) {
     static_assert(LPI == 1 || (LPI == 2 && NPL == 2 && K % 2 == 0), "lane split: two planes, even K");
     constexpr int NP = NPL / LPI;  // planes per lane
     const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = threadIdx.x & 31;
@@ -224,6 +273,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         }
         const uint32_t Dm = valid ? (U[0] | U[1] | U[2] | U[3]) : 0u;
         const uint32_t act = ~Dm;
+        if (base == warp * C.RW) SDIAG(qd, 1);
 
         // footprint rows w-1 .. w+2 of this group (this lane's planes)
         uint32_t Q[4][NP][4];
@@ -295,6 +345,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         ESCG_PUT(2, 0) ESCG_PUT(2, 1) ESCG_PUT(2, 2) ESCG_PUT(2, 3)
         ESCG_PUT(3, 1) ESCG_PUT(3, 2)
 #undef ESCG_PUT
+        if (base == warp * C.RW) SDIAG(qd, 2);
         if (valid) {
 #pragma unroll
             for (int rr = 0; rr < 4; ++rr)
@@ -320,7 +371,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
             if (slot < C.qcap) {
                 C.q[slot] = make_uint4(static_cast<uint32_t>(w) | (static_cast<uint32_t>(acol) << 16), code, item, 0u);
             } else {  // queue full: replay in place (the tile's footprint is disjoint from every other)
-                slice_replay<NPL>(C.sw0, C.RP, C.Gw, w, acol, code, item, l, c1, c2r, C.s32, C.xm, C.xi, C.TK, C.sT,
+                slice_replay_ool<NPL>(C.sw0, C.RP, C.Gw, w, acol, code, item, l, c1, c2r, C.s32, C.xm, C.xi, C.TK, C.sT,
                                   C.S1);
             }
         }
@@ -330,14 +381,16 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
 // The phase's replay pass: queued deferred tiles, one per thread (after the bulk barrier), dealt
 // round-robin over the warps so that each warp runs few (divergent) replays side by side.
 template <int NPL>
-__device__ __forceinline__ void slice_replay_queue(const SliceCtx& C, unsigned n, uint32_t c1, uint32_t c2r) {
+__device__ __forceinline__ void slice_replay_queue(const SliceCtx& C, unsigned n, uint32_t c1, uint32_t c2r,
+                                                   int qd = 0) {
     n = n < C.qcap ? n : C.qcap;
     const unsigned nw = blockDim.x >> 5;
     for (unsigned i = (threadIdx.x & 31) * nw + (threadIdx.x >> 5); i < n; i += blockDim.x) {
         const uint4 e = C.q[i];
         const int w = static_cast<int>(e.x & 0xFFFFu), acol = static_cast<int>(e.x >> 16);
         slice_replay<NPL>(C.sw0, C.RP, C.Gw, w, acol, e.y, e.z, (acol >> 2) & 31, c1, c2r, C.s32, C.xm, C.xi, C.TK,
-                          C.sT, C.S1);
+                          C.sT, C.S1, qd);
+        if (i < nw) SDIAG(qd, 7);
     }
 }
 
@@ -423,16 +476,19 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
                 // before this phase's predecessor's barrier, so it can be zeroed now
                 C.qn = &sQn[q % 3];
                 if (tid == 0) sQn[(q + 1) % 3] = 0u;
+                SDIAG(q, 0);
                 switch (xr) {
-                    case 0: slice_phase<NPL, K, 0, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
-                    case 1: slice_phase<NPL, K, 1, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
-                    case 2: slice_phase<NPL, K, 2, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
-                    default: slice_phase<NPL, K, 3, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r); break;
+                    case 0: slice_phase<NPL, K, 0, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r, q); break;
+                    case 1: slice_phase<NPL, K, 1, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r, q); break;
+                    case 2: slice_phase<NPL, K, 2, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r, q); break;
+                    default: slice_phase<NPL, K, 3, LPI>(C, rp.oy, yr, i_lo, nrows, c1, c2s, c2r, q); break;
                 }
+                SDIAG(q, 3);
                 __syncthreads();
+                SDIAG(q, 4);
                 const unsigned nq = sQn[q % 3];
                 if (nq != 0u) {  // uniform
-                    slice_replay_queue<NPL>(C, nq, c1, c2r);
+                    slice_replay_queue<NPL>(C, nq, c1, c2r, q);
                     __syncthreads();
                 }
             }
@@ -614,6 +670,21 @@ cudaError_t slice_launch_npl(const BlockArgs& a, int nrep, cudaStream_t s) {
 }  // namespace
 
 int slice_row_words(int npl, int gw) { return row_words(npl, gw); }
+
+// Diagnostic: copy the bit-sliced kernel's clock64 stamps (ESCG_DIAG_SLICE builds; else returns -1).
+extern "C" __attribute__((visibility("default"))) int escg_diag_slice(long long* out, int reset) {
+#ifdef ESCG_DIAG_SLICE
+    if (reset) {
+        static long long z[4 * 16 * 8 * 8];
+        return cudaMemcpyToSymbol(g_sdiag, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+    }
+    return cudaMemcpyFromSymbol(out, g_sdiag, sizeof(long long) * 4 * 16 * 8 * 8) == cudaSuccess ? 0 : -1;
+#else
+    (void)out;
+    (void)reset;
+    return -1;
+#endif
+}
 
 cudaError_t launch_slice(const BlockArgs& a, int nrep, cudaStream_t s) {
     if (a.npl == 2 && a.lpi == 2) return slice_launch_npl<2, 2>(a, nrep, s);
