@@ -28,6 +28,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "crs.cuh"
 #include "launch.h"
@@ -378,18 +379,104 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
     }
 }
 
-// The phase's replay pass: queued deferred tiles, one per thread (after the bulk barrier), dealt
-// round-robin over the warps so that each warp runs few (divergent) replays side by side.
+// Group replay: the 8 lanes of group (lane >> 3) replay one tile together.  Lane j reads and writes
+// footprint positions j and j + 8 (the 24 shared-memory reads and up to 24 XOR reductions of a
+// tile are spread over the group); the packed cells are OR-combined with shuffles, and every lane
+// of the group runs the four attempts on the same register copy (the exact rule, branch-free).
+template <int NPL>
+__device__ __forceinline__ void slice_replay_group(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code,
+                                                   uint32_t item, int l, uint32_t c1, uint32_t c2r, uint32_t s32,
+                                                   uint32_t xm, uint32_t xi, uint32_t TK, uint32_t sT, int S1,
+                                                   bool active) {
+    constexpr int CB = NPL == 2 ? 2 : 3;  // bits per packed cell
+    using Pack = typename std::conditional<NPL == 2, uint32_t, uint64_t>::type;
+    constexpr uint32_t kCellPos = 0x8473u;
+    constexpr uint64_t kNbrPos = 0x95847362b8a74130ull;
+    constexpr uint32_t kRow = 0xFAA550u;  // 2-bit row offset + 1 of position k: 0 0 1 1 1 1 2 2 2 2 3 3
+    constexpr uint32_t kCol = 0x9E4E49u;  // 2-bit column offset + 1 of position k: 1 2 0 1 2 3 0 1 2 3 1 2
+    const int j = threadIdx.x & 7;
+    const bool ok = active && acol >= 1 && acol + 2 < 128 * Gw;  // window edge: margin cells, skipped
+    const uint32_t PS = static_cast<uint32_t>(Gw) * 16u;
+    uint32_t addr[2] = {0u, 0u}, bit[2] = {0u, 0u};
+    Pack part = 0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int k = j + 8 * t;
+        if (ok && k < 12) {
+            const int rr = static_cast<int>((kRow >> (2 * k)) & 3u);
+            const int cc = static_cast<int>((kCol >> (2 * k)) & 3u);
+            const int row = w - 1 + rr, col = acol - 1 + cc;
+            addr[t] = sw0 + 4u * static_cast<uint32_t>(row * RP + (col >> 7) * 4 + (col & 3));
+            bit[t] = (static_cast<uint32_t>(col) >> 2) & 31u;
+            uint32_t v = 0;
+#pragma unroll
+            for (int p = 0; p < NPL; ++p) v |= ((lds32(addr[t] + p * PS) >> bit[t]) & 1u) << p;
+            part |= static_cast<Pack>(v) << (CB * k);
+        }
+    }
+    Pack cells = part;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        if constexpr (NPL == 2) {
+            cells |= __shfl_xor_sync(kFull, cells, o);
+        } else {
+            const uint32_t lo = __shfl_xor_sync(kFull, static_cast<uint32_t>(cells), o);
+            const uint32_t hi = __shfl_xor_sync(kFull, static_cast<uint32_t>(cells >> 32), o);
+            cells |= (static_cast<uint64_t>(hi) << 32) | lo;
+        }
+    }
+    if (!ok) return;
+    const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);
+    const Pack cells0 = cells;
+    const uint32_t rw[4] = {rf.x, rf.y, rf.z, rf.w};
+    constexpr Pack M = (static_cast<Pack>(1) << CB) - 1;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const uint32_t cb = (code >> (4 * a)) & 15u;
+        const uint32_t ps = (kCellPos >> (4 * (cb & 3u))) & 15u, pn = static_cast<uint32_t>(kNbrPos >> (4 * cb)) & 15u;
+        const uint32_t s = static_cast<uint32_t>(cells >> (CB * ps)) & M, n = static_cast<uint32_t>(cells >> (CB * pn)) & M;
+        const bool und = (code >> (16 + a)) & 1u;
+        const uint32_t x = TK | (rw[a] & ~TK);
+        const bool mig = !und || x < xm, rep = und && x >= xi;
+        const bool inter = !mig && !rep && s != 0u && n != 0u && s != n;
+        const uint32_t t1 = lds32_if(inter, sT + 4u * (s * S1 + n), 0u);
+        const uint32_t t2 = lds32_if(inter, sT + 4u * (n * S1 + s), 0u);
+        const bool kn = inter && x < t1, ks = inter && !(x < t1) && x < t2;
+        const bool r1 = rep && n == 0u, r2 = rep && n != 0u && s == 0u;
+        const uint32_t ns = mig ? n : (ks ? 0u : (r2 ? n : s));
+        const uint32_t nn = mig ? s : (kn ? 0u : (r1 ? s : n));
+        cells = (cells & ~((M << (CB * ps)) | (M << (CB * pn)))) | (static_cast<Pack>(ns) << (CB * ps)) |
+                (static_cast<Pack>(nn) << (CB * pn));
+    }
+    const Pack delta = cells ^ cells0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        const int k = j + 8 * t;
+        if (k < 12) {
+#pragma unroll
+            for (int p = 0; p < NPL; ++p)
+                if ((delta >> (CB * k + p)) & 1u)
+                    asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[t] + p * PS), "r"(1u << bit[t]) : "memory");
+        }
+    }
+}
+
+// The phase's replay pass: queued deferred tiles, one per 8-lane group (after the bulk barrier),
+// dealt round-robin over the warps.
 template <int NPL>
 __device__ __forceinline__ void slice_replay_queue(const SliceCtx& C, unsigned n, uint32_t c1, uint32_t c2r,
                                                    int qd = 0) {
     n = n < C.qcap ? n : C.qcap;
-    const unsigned nw = blockDim.x >> 5;
-    for (unsigned i = (threadIdx.x & 31) * nw + (threadIdx.x >> 5); i < n; i += blockDim.x) {
-        const uint4 e = C.q[i];
+    const unsigned nw = blockDim.x >> 5, ng = blockDim.x >> 3;
+    const unsigned g0 = ((threadIdx.x & 31) >> 3) * nw + (threadIdx.x >> 5);  // group index, warps first
+    for (unsigned base = 0; base < n; base += ng) {  // uniform
+        const unsigned i = base + g0;
+        const bool act = i < n;
+        uint4 e = make_uint4(0u, 0u, 0u, 0u);
+        if (act) e = C.q[i];
         const int w = static_cast<int>(e.x & 0xFFFFu), acol = static_cast<int>(e.x >> 16);
-        slice_replay<NPL>(C.sw0, C.RP, C.Gw, w, acol, e.y, e.z, (acol >> 2) & 31, c1, c2r, C.s32, C.xm, C.xi, C.TK,
-                          C.sT, C.S1, qd);
+        slice_replay_group<NPL>(C.sw0, C.RP, C.Gw, w, acol, e.y, e.z, (acol >> 2) & 31, c1, c2r, C.s32, C.xm, C.xi,
+                                C.TK, C.sT, C.S1, act);
         if (i < nw) SDIAG(qd, 7);
     }
 }
