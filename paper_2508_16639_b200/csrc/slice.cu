@@ -396,6 +396,7 @@ __device__ __forceinline__ void slice_replay_group(uint32_t sw0, int RP, int Gw,
     constexpr uint32_t kCol = 0x9E4E49u;  // 2-bit column offset + 1 of position k: 1 2 0 1 2 3 0 1 2 3 1 2
     const int j = threadIdx.x & 7;
     const bool ok = active && acol >= 1 && acol + 2 < 128 * Gw;  // window edge: margin cells, skipped
+    const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);  // overlaps the reads
     const uint32_t PS = static_cast<uint32_t>(Gw) * 16u;
     uint32_t addr[2] = {0u, 0u}, bit[2] = {0u, 0u};
     Pack part = 0;
@@ -426,7 +427,6 @@ __device__ __forceinline__ void slice_replay_group(uint32_t sw0, int RP, int Gw,
         }
     }
     if (!ok) return;
-    const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);
     const Pack cells0 = cells;
     const uint32_t rw[4] = {rf.x, rf.y, rf.z, rf.w};
     constexpr Pack M = (static_cast<Pack>(1) << CB) - 1;
