@@ -79,9 +79,20 @@ def reference_sample(mcs, mode=2, workers=None, seed=1):
 def cpu_baseline():
     # ~10 s wall on 16 host cores (~2e8 attempts/s): a bounded sample of the L=3200 workload
     v, el, w = reference_sample(mcs=200, mode=2)
-    return {"value": v, "unit": UNIT, "cores": w, "kind": "reference",
-            "sample": "reference run_max_step (ThreadPool(%d)), RPS L=3200 M=1e-4 p0=0.1, 200 MCS window "
-                      "from the first density record (%.1f s wall)" % (w, el)}
+    out = {"value": v, "unit": UNIT, "cores": w, "kind": "reference",
+           "sample": "reference run_max_step (ThreadPool(%d)), RPS L=3200 M=1e-4 p0=0.1, 200 MCS window "
+                     "from the first density record (%.1f s wall)" % (w, el)}
+    # SURVEY §8d's single-core comparison: run_serial (EngineMode::Serial) pinned to one core, ~8 s
+    aff = os.sched_getaffinity(0)
+    try:
+        os.sched_setaffinity(0, {min(aff)})
+        sv, sel, _ = reference_sample(mcs=6, mode=0)
+    finally:
+        os.sched_setaffinity(0, aff)
+    out["serial"] = {"value": sv, "unit": UNIT, "cores": 1, "kind": "reference",
+                     "sample": "reference run_serial pinned to core %d, RPS L=3200 M=1e-4 p0=0.1, 6 MCS window "
+                               "(%.1f s wall)" % (min(aff), sel)}
+    return out
 
 
 def run_reference_arm(args):

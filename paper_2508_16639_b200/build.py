@@ -36,20 +36,26 @@ def build(force: bool = False, verbose: bool = False, out: str = None, defines=(
     if out is None and not defines and not force and not _stale():
         return LIB
     objs = []
-    logs = []
-    for src in SOURCES:
+    procs = []
+    for src in SOURCES:  # the translation units compile in parallel
         obj = os.path.join(CSRC, src + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, *["-D" + d for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
                os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd.insert(1, "-x")
             cmd.insert(2, "cu")
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        logs.append(r.stdout + r.stderr)
-        if r.returncode != 0:
-            sys.stderr.write(r.stdout + r.stderr)
-            raise RuntimeError("nvcc failed on %s" % src)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
         objs.append(obj)
+    logs = []
+    failed = None
+    for src, pr in procs:
+        out = pr.communicate()[0]
+        logs.append(out)
+        if pr.returncode != 0:
+            sys.stderr.write(out)
+            failed = failed or src
+    if failed:
+        raise RuntimeError("nvcc failed on %s" % failed)
     tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xlinker", "--exclude-libs,ALL"]
     r = subprocess.run(cmd, capture_output=True, text=True)

@@ -574,7 +574,11 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
                 __syncthreads();
                 SDIAG(q, 4);
                 const unsigned nq = sQn[q % 3];
+#ifdef ESCG_DIAG_SLICE_NOREPLAY  // diagnostic builds only: skips the replay pass (wrong results)
+                if (nq == 0x7fffffffu) {
+#else
                 if (nq != 0u) {  // uniform
+#endif
                     slice_replay_queue<NPL>(C, nq, c1, c2r, q);
                     __syncthreads();
                 }

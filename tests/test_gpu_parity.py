@@ -592,7 +592,7 @@ SLICED_CASES = [
 ]
 
 
-@pytest.mark.parametrize("lpi,qcap", [("1", None), ("2", None), ("2", "3")])
+@pytest.mark.parametrize("lpi,qcap", [("1", None), ("1", "1"), ("2", None), ("2", "3")])
 @pytest.mark.parametrize("case", SLICED_CASES, ids=[f"{c[0]}x{c[1]}_{c[5]}_K{c[8]}" for c in SLICED_CASES])
 def test_slice_kernel_matches_crs_oracle(escg, oracle, case, lpi, qcap, monkeypatch):
     """The bit-sliced block kernel == oracle orc_crs_run with the SLICED draw spec, bit for bit:
