@@ -330,7 +330,7 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
     const int regs = (escgd::slice_kernel_registers(h->npl, h->lpi) + 7) / 8 * 8;
     const int cta_per_sm = std::max(1, std::min(4, 65536 / std::max(1, regs * nthr)));
     sms *= cta_per_sm;
-    const int GL = h->L / 128, uy = h->H / 4;
+    const int GL = h->L / 128, uy = h->rows_count / 4;  // band engines: the band's rows only
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
     double overhead = 20000.0;  // launch + window load/store, in cell units
@@ -377,7 +377,7 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
     h->nbx = bnbx;
     h->kmcs = bk;
     std::vector<int> rows(bnby + 1), cols(bnbx + 1);
-    for (int i = 0; i <= bnby; ++i) rows[i] = static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
+    for (int i = 0; i <= bnby; ++i) rows[i] = h->rows_begin + static_cast<int>(static_cast<int64_t>(uy) * i / bnby) * 4;
     for (int i = 0; i <= bnbx; ++i) cols[i] = static_cast<int>(static_cast<int64_t>(GL) * i / bnbx);
     int bh = 0, gw = 0;
     for (int i = 0; i < bnby; ++i) bh = std::max(bh, rows[i + 1] - rows[i]);
@@ -909,13 +909,13 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             }
         }
         // SLICED (bit-sliced block kernel, slice.cu): periodic von Neumann lattices with L % 128 == 0,
-        // S <= 7, single-band engines, when at least 6 leading bits of X_mig are ones: K (even, <= 16,
+        // S <= 7 (row-band engines too), when at least 6 leading bits of X_mig are ones: K (even, <= 16,
         // <= those bits) action planes make every word with a zero among its top K bits a certain
         // migration.  Chosen by default from 8 leading ones (P(migration) >= 0.996).
         {
             int lead = 0;
             while (lead < 32 && ((h->th.xm >> (31 - lead)) & 1u)) ++lead;
-            const bool ok = choice == ESCG_KERNEL_BLOCK && !bs && periodic4 && h->arity == 4 && h->L % 128 == 0 &&
+            const bool ok = choice == ESCG_KERNEL_BLOCK && periodic4 && h->arity == 4 && h->L % 128 == 0 &&
                             h->S <= 7 && lead >= 6;
             bool use = ok && lead >= 8;
             if (const char* f = std::getenv("ESCG_DRAW_FORMAT")) use = ok && std::strcmp(f, "sliced") == 0;
@@ -1285,6 +1285,8 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
             if (!h || h->nbands != n || h->band != g) config_error("group must list bands 0..n-1 of one lattice");
             if (h->mcs[0] != bands[0]->mcs[0] || h->cur[0] != bands[0]->cur[0] || h->kmcs != bands[0]->kmcs)
                 config_error("bands are out of step");
+            if (h->narrow != bands[0]->narrow || h->K != bands[0]->K || h->npl != bands[0]->npl)
+                config_error("bands must share one draw format");
         }
         // peer access between ring neighbours on different GPUs (NVLink P2P copies)
         for (int g = 0; g < n; ++g) {
@@ -1321,12 +1323,19 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
             CK(cudaSetDevice(bands[g]->device));
             CK(cudaEventCreateWithFlags(&ev_k[g], cudaEventDisableTiming));
             CK(cudaEventCreateWithFlags(&ev_x[g], cudaEventDisableTiming));
-            CK(cudaEventRecord(ev_k[g], bands[g]->stream));
         }
         const int64_t t0 = bands[0]->mcs[0];
         int64_t launch_no = 0;
         int par = bands[0]->cur[0];
         const int k = bands[0]->kmcs;
+        // bit-sliced bands stay in plane form for the whole call: halos move as plane rows
+        const bool sliced = bands[0]->narrow == 2 && n_mcs > 0;
+        for (int g = 0; g < n; ++g) {
+            escg_dev* h = bands[g];
+            CK(cudaSetDevice(h->device));
+            if (sliced) CK(escgd::launch_to_planes(h->lat[par].p, h->pl[par].p, h->H, h->L, h->npl, 1, h->stream));
+            CK(cudaEventRecord(ev_k[g], h->stream));
+        }
         for (int64_t done = 0; done < n_mcs;) {
             const int chunk = static_cast<int>(std::min<int64_t>(k, n_mcs - done));
             // halo exchange into buffer `par` (reads the neighbours' band rows of buffer `par`)
@@ -1337,16 +1346,19 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 CK(cudaSetDevice(h->device));
                 CK(cudaStreamWaitEvent(h->stream, ev_k[(g + n - 1) % n], 0));
                 CK(cudaStreamWaitEvent(h->stream, ev_k[(g + 1) % n], 0));
-                const size_t rowb = static_cast<size_t>(h->L);
+                // a row: L bytes, or NPL planes x L/128 groups x 4 words when bit-sliced
+                const size_t rowb = sliced ? static_cast<size_t>(h->npl) * (h->L / 128) * 16 : static_cast<size_t>(h->L);
                 const size_t hb = static_cast<size_t>(h->halo) * rowb;
-                uint8_t* mine = h->lat[par].p;
+                auto buf = [&](escg_dev* e) {
+                    return sliced ? reinterpret_cast<uint8_t*>(e->pl[par].p) : e->lat[par].p;
+                };
+                uint8_t* mine = buf(h);
                 // top halo ← the last `halo` rows of the band above; bottom halo ← the first rows below
                 CK(cudaMemcpyPeerAsync(mine, h->device,
-                                       up->lat[par].p + static_cast<size_t>(up->halo + up->band_rows - h->halo) * rowb,
+                                       buf(up) + static_cast<size_t>(up->halo + up->band_rows - h->halo) * rowb,
                                        up->device, hb, h->stream));
                 CK(cudaMemcpyPeerAsync(mine + static_cast<size_t>(h->halo + h->band_rows) * rowb, h->device,
-                                       dn->lat[par].p + static_cast<size_t>(dn->halo) * rowb, dn->device, hb,
-                                       h->stream));
+                                       buf(dn) + static_cast<size_t>(dn->halo) * rowb, dn->device, hb, h->stream));
                 CK(cudaEventRecord(ev_x[g], h->stream));
             }
             // chunk: src = buffer par, dst = 1 - par.  A band's kernel overwrites buffer 1-par, which
@@ -1384,11 +1396,20 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 a.count = 0;
                 a.src = h->lat[par].p;
                 a.dst = h->lat[1 - par].p;
+                a.psrc = h->pl[par].p;
+                a.pdst = h->pl[1 - par].p;
+                a.K = h->K;
+                a.npl = h->npl;
+                a.lpi = h->lpi;
+                a.qcap = h->qcap;
                 a.dst_index = 1 - par;
                 a.mcs = t0 + done;
                 a.nmcs = chunk;
                 CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
-                CK(escgd::launch_block(a, 1, h->threads, h->stream));
+                if (sliced)
+                    CK(escgd::launch_slice(a, 1, h->stream));
+                else
+                    CK(escgd::launch_block(a, 1, h->threads, h->stream));
                 CK(cudaEventRecord(ev_k[g], h->stream));
             }
             par ^= 1;
@@ -1397,6 +1418,9 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
         }
         for (int g = 0; g < n; ++g) {
             CK(cudaSetDevice(bands[g]->device));
+            if (sliced)
+                CK(escgd::launch_from_planes(bands[g]->pl[0].p, bands[g]->pl[1].p, nullptr, par, bands[g]->lat[par].p,
+                                             bands[g]->H, bands[g]->L, bands[g]->npl, 1, bands[g]->stream));
             CK(cudaStreamSynchronize(bands[g]->stream));
             bands[g]->mcs[0] += n_mcs;
             bands[g]->cur[0] = par;
@@ -1454,11 +1478,25 @@ int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
         a.count = 0;
         a.src = h->lat[par].p;
         a.dst = h->lat[1 - par].p;
+        a.psrc = h->pl[par].p;
+        a.pdst = h->pl[1 - par].p;
+        a.K = h->K;
+        a.npl = h->npl;
+        a.lpi = h->lpi;
+        a.qcap = h->qcap;
         a.dst_index = 1 - par;
         a.mcs = h->mcs[0];
         a.nmcs = n_mcs;
         CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
-        CK(escgd::launch_block(a, 1, h->threads, h->stream));
+        if (h->narrow == 2) {
+            // bit-sliced: the halos arrive as bytes (escg_dev_band_rows), so each step converts
+            CK(escgd::launch_to_planes(h->lat[par].p, h->pl[par].p, h->H, h->L, h->npl, 1, h->stream));
+            CK(escgd::launch_slice(a, 1, h->stream));
+            CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, 1 - par, h->lat[1 - par].p, h->H, h->L,
+                                         h->npl, 1, h->stream));
+        } else {
+            CK(escgd::launch_block(a, 1, h->threads, h->stream));
+        }
         CK(cudaStreamSynchronize(h->stream));
         h->cur[0] = 1 - par;
         h->mcs[0] += n_mcs;

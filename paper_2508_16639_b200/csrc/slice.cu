@@ -489,13 +489,14 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     __shared__ unsigned sQn[3];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int r = blockIdx.z, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    // local rows (the buffer; band engines: halo + band + halo, never wrapped) vs global rows (draws)
     const int Hg = a.H, GL = a.L >> 7, S1 = a.S + 1;
     const int My = margin_rows(a.nmcs);
     const int ry0 = a.row_split[blockIdx.y], ry1 = a.row_split[blockIdx.y + 1];
     const int gs0 = a.col_split[blockIdx.x], gs1 = a.col_split[blockIdx.x + 1];
     const int Gw = gs1 - gs0 + 1, bh = ry1 - ry0, Wh = bh + 2 * My;
     const int RP = row_words(NPL, Gw), per_row = NPL * Gw;
-    const int wy0 = ((ry0 - My) % Hg + Hg) % Hg;
+    const int wy0 = a.wrap_rows ? ((ry0 - My) % Hg + Hg) % Hg : ry0 - My;  // bands: halo rows, no wrap
     const bool bigy = Wh > Hg;
     const size_t NW = static_cast<size_t>(Hg) * NPL * GL * 4;
     const uint32_t* src = a.psrc + r * NW;
@@ -531,9 +532,9 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
         C.gw = lane / LPI - C.tr * Gw;
         C.gs0 = gs0;
         C.GL = GL;
-        C.Hg = Hg;
-        C.wy0 = wy0;
-        C.bigy = bigy;
+        C.Hg = a.Hg;                   // draws use global rows: local row r is global (row0 + r) mod Hg
+        C.wy0 = (a.row0 + wy0) % a.Hg;
+        C.bigy = Wh > a.Hg;
         C.s32 = seed32(a.seeds[r]);
         C.xm = a.rule.xm;
         C.xi = a.rule.xi;

@@ -347,6 +347,76 @@ def test_band_group_equals_single_lattice(escg, oracle, n_bands, kmcs, LH):
     assert np.array_equal(single, oracle.crs_run(init, L, H, model.matrix(), 1e-2, 555, 0, 7, narrow=narrow))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_bands,kmcs,L,H,S", [(2, 1, 256, 128, 3), (3, 2, 384, 240, 3), (4, 2, 128, 208, 5)])
+def test_sliced_band_group_equals_single_lattice(escg, oracle, n_bands, kmcs, L, H, S, monkeypatch):
+    """Row bands on the bit-sliced kernel: the group stays in plane form across chunks (halos move as
+    plane rows) and equals the single-lattice bit-sliced run and the oracle's SLICED schedule."""
+    from paper_2508_16639_b200.bands import BandGroup
+
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    model = escg.make_circulant(3, [1]) if S == 3 else escg.make_rpsls()
+    p = params(escg, L, H, S, 1e-2, 0.1, 4, True, seed=808)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        assert eng.draw_format() == "sliced"
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(9)
+        single = eng.get_lattice()
+        narrow = eng.draw_code()
+    with BandGroup(p, model, n_bands, kmcs=kmcs) as grp:
+        grp.init_lattice()
+        grp.advance(4)
+        grp.advance(5)
+        banded = grp.get_lattice()
+        assert np.array_equal(grp.counts(), np.bincount(banded, minlength=S + 1).astype(np.uint64))
+    assert np.array_equal(banded, single)
+    assert np.array_equal(single, oracle.crs_run(init, L, H, model.matrix(), 1e-2, 808, 0, 9, narrow=narrow))
+
+
+@pytest.mark.gpu
+def test_sliced_band_primitives_match_single_lattice(escg, monkeypatch):
+    """The multi-process band path (escg_dev_band_rows + escg_dev_band_step, byte halos) on the
+    bit-sliced kernel, bands in one process: equals the single-lattice run bit for bit."""
+    import torch
+
+    from paper_2508_16639_b200._lib import check, lib
+    from paper_2508_16639_b200.bands import DistributedBand
+
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    L, H, n_bands, kmcs = 256, 192, 3, 2
+    p = params(escg, L, H, 3, 1e-2, 0.1, 4, True, seed=32)
+    model = escg.make_circulant(3, [1])
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        assert eng.draw_format() == "sliced"
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(7)
+        want = eng.get_lattice()
+    bands = [DistributedBand(p, model, rank=g, world=n_bands, device=0, kmcs=kmcs) for g in range(n_bands)]
+    try:
+        for b in bands:
+            s, r = b.info["start"], b.info["rows"]
+            b.set_band(init[s * L:(s + r) * L], 0)
+        done = 0
+        while done < 7:
+            chunk = min(kmcs, 7 - done)
+            views = [b.halo_views() for b in bands]
+            for g in range(n_bands):
+                up, dn = views[(g - 1) % n_bands], views[(g + 1) % n_bands]
+                views[g][0].copy_(up[2])
+                views[g][3].copy_(dn[1])
+            torch.cuda.synchronize()
+            for b in bands:
+                check(lib().escg_dev_band_step(b._h, chunk))
+            done += chunk
+        got = np.concatenate([b.get_band() for b in bands])
+        assert np.array_equal(got, want)
+    finally:
+        for b in bands:
+            b.close()
+
+
 def test_band_group_resume_from_host_lattice(escg):
     from paper_2508_16639_b200.bands import BandGroup
 
