@@ -208,6 +208,7 @@ struct escg_dev {
     std::vector<int> cur;      // block path: buffer holding replica r's lattice
     DevBuf<uint8_t> lat[2];
     DevBuf<uint32_t> pl[2];  // SLICED: bit-plane lattices during run/advance (slice.cu)
+    bool planes_live = false;  // SLICED band engines between band steps: the state is pl[cur], not lat[cur]
     DevBuf<uint64_t> d_seeds, d_last;
     DevBuf<uint32_t> d_T;
     DevBuf<int64_t> d_mcs, d_nrec, d_tsteps;
@@ -445,6 +446,21 @@ uint8_t* replica_lat(escg_dev* h, int r) {
 // The rows an engine owns (whole lattice, or the band of a band engine): I/O and counts use these.
 uint8_t* owned_lat(escg_dev* h, int r) { return replica_lat(h, r) + static_cast<size_t>(h->rows_begin) * h->L; }
 int64_t owned_cells(escg_dev* h) { return static_cast<int64_t>(h->rows_count) * h->L; }
+
+// Bit-sliced band engines stepped one process per GPU (escg_dev_band_rows / escg_dev_band_step)
+// stay in plane form between steps; byte readers convert back first.
+void band_sync_bytes(escg_dev* h) {
+    if (!h->planes_live) return;
+    const int c = h->cur[0];
+    CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, c, h->lat[c].p, h->H, h->L, h->npl, 1, h->stream));
+    h->planes_live = false;
+}
+void band_sync_planes(escg_dev* h) {
+    if (h->planes_live) return;
+    const int c = h->cur[0];
+    CK(escgd::launch_to_planes(h->lat[c].p, h->pl[c].p, h->H, h->L, h->npl, 1, h->stream));
+    h->planes_live = true;
+}
 
 void check_replica(escg_dev* h, int r) {
     if (r < 0 || r >= h->nrep) config_error("replica index out of range");
@@ -1024,6 +1040,7 @@ int escg_dev_init_lattice(escg_dev* h) {
         CK(cudaStreamSynchronize(h->stream));
         std::fill(h->mcs.begin(), h->mcs.end(), 0);
         std::fill(h->cur.begin(), h->cur.end(), 0);
+        h->planes_live = false;
     });
 }
 
@@ -1043,6 +1060,7 @@ int escg_dev_set_lattice(escg_dev* h, int32_t replica, const int32_t* cells, int
         CK(cudaStreamSynchronize(h->stream));
         if (bad) throw Error(ESCG_EENGINE, "corrupt lattice value (outside [0, S])");
         h->mcs[replica] = mcs;
+        h->planes_live = false;
     });
 }
 
@@ -1051,6 +1069,7 @@ int escg_dev_get_lattice(escg_dev* h, int32_t replica, int32_t* out, int64_t* mc
         if (!h) config_error("null handle");
         check_replica(h, replica);
         CK(cudaSetDevice(h->device));
+        band_sync_bytes(h);
         if (out) {
             const int64_t n = owned_cells(h);
             if (h->d_i32.n < static_cast<size_t>(n)) h->d_i32.alloc(n);
@@ -1067,6 +1086,7 @@ int escg_dev_counts(escg_dev* h, int32_t replica, uint64_t* out) {
         if (!h || !out) config_error("null argument");
         check_replica(h, replica);
         CK(cudaSetDevice(h->device));
+        band_sync_bytes(h);
         DevBuf<unsigned long long> tmp;
         tmp.alloc(h->S1);
         CK(escgd::launch_count(owned_lat(h, replica), owned_cells(h), 1, h->S, tmp.p, h->stream));
@@ -1333,7 +1353,7 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
         for (int g = 0; g < n; ++g) {
             escg_dev* h = bands[g];
             CK(cudaSetDevice(h->device));
-            if (sliced) CK(escgd::launch_to_planes(h->lat[par].p, h->pl[par].p, h->H, h->L, h->npl, 1, h->stream));
+            if (sliced) band_sync_planes(h);
             CK(cudaEventRecord(ev_k[g], h->stream));
         }
         for (int64_t done = 0; done < n_mcs;) {
@@ -1418,9 +1438,10 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
         }
         for (int g = 0; g < n; ++g) {
             CK(cudaSetDevice(bands[g]->device));
-            if (sliced)
-                CK(escgd::launch_from_planes(bands[g]->pl[0].p, bands[g]->pl[1].p, nullptr, par, bands[g]->lat[par].p,
-                                             bands[g]->H, bands[g]->L, bands[g]->npl, 1, bands[g]->stream));
+            if (sliced) {
+                bands[g]->cur[0] = par;
+                band_sync_bytes(bands[g]);
+            }
             CK(cudaStreamSynchronize(bands[g]->stream));
             bands[g]->mcs[0] += n_mcs;
             bands[g]->cur[0] = par;
@@ -1434,13 +1455,20 @@ int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint
     return guarded([&] {
         if (!h) config_error("null handle");
         if (h->nbands < 2) config_error("not a band engine");
+        CK(cudaSetDevice(h->device));
         uint8_t* base = h->lat[h->cur[0]].p;
-        const size_t row = static_cast<size_t>(h->L);
+        size_t row = static_cast<size_t>(h->L);
+        if (h->narrow == 2) {  // bit-sliced: halos move as plane rows (NPL x L/128 x 16 bytes)
+            band_sync_planes(h);
+            CK(cudaStreamSynchronize(h->stream));
+            base = reinterpret_cast<uint8_t*>(h->pl[h->cur[0]].p);
+            row = static_cast<size_t>(h->npl) * (h->L / 128) * 16;
+        }
         if (recv_top) *recv_top = base;
         if (send_top) *send_top = base + static_cast<size_t>(h->halo) * row;
         if (send_bot) *send_bot = base + static_cast<size_t>(h->band_rows) * row;
         if (recv_bot) *recv_bot = base + static_cast<size_t>(h->halo + h->band_rows) * row;
-        if (bytes) *bytes = static_cast<int64_t>(h->halo) * h->L;
+        if (bytes) *bytes = static_cast<int64_t>(h->halo * row);
     });
 }
 
@@ -1488,12 +1516,9 @@ int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
         a.mcs = h->mcs[0];
         a.nmcs = n_mcs;
         CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
-        if (h->narrow == 2) {
-            // bit-sliced: the halos arrive as bytes (escg_dev_band_rows), so each step converts
-            CK(escgd::launch_to_planes(h->lat[par].p, h->pl[par].p, h->H, h->L, h->npl, 1, h->stream));
+        if (h->narrow == 2) {  // bit-sliced: the band stays in plane form between steps
+            band_sync_planes(h);
             CK(escgd::launch_slice(a, 1, h->stream));
-            CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, 1 - par, h->lat[1 - par].p, h->H, h->L,
-                                         h->npl, 1, h->stream));
         } else {
             CK(escgd::launch_block(a, 1, h->threads, h->stream));
         }
