@@ -167,7 +167,9 @@ ESCG_API int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs);
 /* Primitives of a multi-process band group (one rank per GPU, halos moved by the caller, e.g. NCCL
  * send/recv): device pointers into the band's current buffer — the top halo rows, the first
  * `halo` band rows (sent up), the last `halo` band rows (sent down), the bottom halo rows — and the
- * byte count of each (halo * L).  Valid until the next escg_dev_band_step. */
+ * byte count of each: halo * L for u8 rows, halo * NPL * L/128 * 16 when the band runs the
+ * bit-sliced kernel (draw format 2: the band stays in bit-plane rows between steps, and
+ * get/counts convert back on demand).  Valid until the next escg_dev_band_step. */
 ESCG_API int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint8_t** send_bot,
                                 uint8_t** recv_bot, int64_t* bytes);
 /* One chunk (1 <= n_mcs <= kmcs) of MCS on this band alone; the halos must hold the neighbours'
