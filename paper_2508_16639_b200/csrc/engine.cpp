@@ -938,6 +938,10 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             if (use) {
                 h->narrow = 2;
                 h->K = std::min(lead, escgd::kSliceMaxK) & ~1;
+                if (const char* kv = std::getenv("ESCG_SLICE_K")) {  // experiments: fewer action planes
+                    const int kf = std::atoi(kv) & ~1;
+                    if (kf >= 6 && kf <= h->K) h->K = kf;
+                }
                 h->npl = h->S <= 3 ? 2 : 3;
                 // one lane per item: measured faster than a lane pair at L=3200 (4.8e11 vs 4.3e11) and
                 // even at L=16384 (8.8e11 vs 9.0e11); the pair stays selectable (ESCG_SLICE_LPI=2)
