@@ -148,10 +148,13 @@ cudaError_t launch_replay(const ReplayArgs& a, cudaStream_t s);
 #ifndef ESCG_SLICE_T2
 #define ESCG_SLICE_T2 512
 #endif
+#ifndef ESCG_SLICE_T1  // experiments: CTA size of the one-lane kernel
+#define ESCG_SLICE_T1 256
+#endif
 #ifndef ESCG_SLICE_MINB1  // experiments: CTAs per SM the one-lane kernel is compiled for
 #define ESCG_SLICE_MINB1 1
 #endif
-__host__ __device__ constexpr int slice_threads(int lpi) { return lpi == 2 ? ESCG_SLICE_T2 : 256; }
+__host__ __device__ constexpr int slice_threads(int lpi) { return lpi == 2 ? ESCG_SLICE_T2 : ESCG_SLICE_T1; }
 __host__ __device__ constexpr int slice_min_blocks(int lpi) { return lpi == 2 ? 512 / ESCG_SLICE_T2 : ESCG_SLICE_MINB1; }
 constexpr int kSliceMaxK = 16;
 cudaError_t launch_slice(const BlockArgs& a, int nrep, cudaStream_t s);
