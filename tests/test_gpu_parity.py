@@ -706,6 +706,25 @@ def test_slice_kernel_matches_crs_oracle(escg, oracle, case, lpi, qcap, monkeypa
     assert np.array_equal(fin, cur)
 
 
+@pytest.mark.parametrize("kforce,kwant", [("10", 10), ("7", 6), ("4", 16), ("18", 16)])
+def test_slice_kernel_forced_action_planes(escg, oracle, kforce, kwant, monkeypatch):
+    """ESCG_SLICE_K (experiments) lowers K to an even value in [6, leading ones of X_mig]; anything
+    else is ignored.  The forced format is still the oracle's SLICED definition with that K."""
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    monkeypatch.setenv("ESCG_SLICE_K", kforce)
+    L, H, M = 1024, 256, 1.0  # X_mig has >= 16 leading ones
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, H, 3, M, 0.1, 4, True, seed=29, mcs=4)
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        code = eng.draw_code()
+        assert code == 2 | (kwant << 8), hex(code)
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(3)
+        got = eng.get_lattice()
+    assert np.array_equal(got, oracle.crs_run(init, L, H, model.matrix(), M, 29, 0, 3, narrow=code))
+
+
 def test_slice_kernel_replicas_and_stops(escg, oracle, monkeypatch):
     """Replica batches on the bit-sliced kernel: every replica equals its single run; a tracked
     extinction stop leaves the lattice of the stopping record (plane buffer named by `cur`)."""
