@@ -232,6 +232,10 @@ def run_ours(args):
         m0 = eng.mcs()
         st = eng.run(m0 + MCS_PER_STEP, interval=interval, record_trace=False)
         ms, launches = eng.last_timing()
+        # a lattice that reached stasis or a stop rule would make later launches no-ops and inflate
+        # the rate: every counted step must complete its full MCS_PER_STEP
+        if int(st[0]) != int(e.RunStatus.Completed) or eng.mcs() != m0 + MCS_PER_STEP:
+            raise RuntimeError("bench step did not complete: status %d, MCS %d -> %d" % (int(st[0]), m0, eng.mcs()))
         return ms, launches, int(st[0])
 
     for _ in range(args.warmup):
@@ -286,6 +290,8 @@ def run_ours(args):
                                      _lib.ptr(lat_out), C.byref(out_mcs), _lib.ptr(steps_buf), _lib.ptr(counts_buf), cap,
                                      C.byref(n_rec), C.byref(status)))
         t1 = time.perf_counter()
+        if status.value != int(e.RunStatus.Completed) or out_mcs.value != cur + MCS_PER_STEP:
+            raise RuntimeError("e2e step did not complete: status %d, MCS %d -> %d" % (status.value, cur, out_mcs.value))
         if i >= args.warmup:
             e2e_times.append(t1 - t0)
         lat_in, lat_out = lat_out, lat_in

@@ -1,5 +1,6 @@
-"""Statistics helpers of the reference library (include/escg/stats.hpp, src/stats.cpp), used by the
-experiments harness and by the acceptance criteria the reference's SPEC states.
+"""Statistics helpers of the reference library (include/escg/stats.hpp, src/stats.cpp) restated as TEST
+INFRASTRUCTURE (SURVEY §2.1 marks stats.cpp out of scope for the product): the statistical parity tests
+use them as checkers.  Nothing in paper_2508_16639_b200/ imports this module.
 
     mean_std(xs)                     stats.cpp:9-21   sample mean and (n-1) standard deviation
     gamma_q(a, x)                    stats.cpp:61-66  regularized upper incomplete gamma Q(a, x)
@@ -13,7 +14,7 @@ from __future__ import annotations
 import math
 from typing import Sequence
 
-from .experiments import MeanStd, mean_std  # noqa: F401  (stats.cpp:9-21 lives with the harness)
+from paper_2508_16639_b200.experiments import MeanStd, mean_std  # noqa: F401  (stats.cpp:9-21 lives with the harness)
 
 _EPS = 1e-15
 _TINY = 1e-300

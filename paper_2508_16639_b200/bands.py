@@ -17,7 +17,7 @@ import numpy as np
 
 from ._lib import check, lib
 from .engine import DominanceModel, SimParams
-from .errors import ConfigError
+from .errors import ConfigError, EngineError
 
 
 def band_rows(height: int, n_bands: int):
@@ -152,6 +152,26 @@ class DistributedBand:
                                          int(kmcs), C.byref(h)))
         self._h = h
         self.info = BandGroup._band_info(h)
+        if self.info["kmcs"] != kmcs:
+            raise EngineError("band engine runs %d MCS per chunk, %d requested" % (self.info["kmcs"], kmcs))
+        self._check_uniform_chunk()
+
+    def _check_uniform_chunk(self):
+        """Every rank must post the same number of halo exchanges per advance: the chunk (kmcs) and
+        halo depth have to agree over the group, else ranks pair stale halos and hang."""
+        import torch
+        import torch.distributed as dist
+
+        if not dist.is_available() or not dist.is_initialized():
+            return
+        backend = dist.get_backend(self.group)
+        dev = torch.device("cuda", self.device) if backend == "nccl" else torch.device("cpu")
+        mine = torch.tensor([self.info["kmcs"], self.info["halo"]], dtype=torch.int64, device=dev)
+        lo, hi = mine.clone(), mine.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.group)
+        if not torch.equal(lo, hi):
+            raise EngineError("band chunk/halo differ across ranks: min %s max %s" % (lo.tolist(), hi.tolist()))
 
     def close(self):
         if self._h:

