@@ -52,6 +52,9 @@ extern "C" {
 #define ESCG_KERNEL_AUTO 0
 #define ESCG_KERNEL_TILE 1  /* whole lattice resident in one CTA's shared memory, persistent  */
 #define ESCG_KERNEL_BLOCK 2 /* overlapped-tile kernel over an HBM/L2-resident lattice          */
+#define ESCG_KERNEL_RING 3  /* persistent bit-sliced row bands (one CTA per SM, L2 boundary mail):
+                               AUTO picks it for single periodic lattices with 1024 <= L <= 4096,
+                               L % 128 == 0 at high mobility (the L=3200 bench) */
 
 /* POD mirror of escg::SimParams (params.hpp:18-49); defaults via escg_params_default(). */
 typedef struct escg_params {
@@ -143,7 +146,7 @@ ESCG_API int escg_dev_replay(escg_dev* h, const uint32_t* w_cell, const uint32_t
  * engine's stream; and the number of kernels that call launched. */
 ESCG_API int escg_dev_last_timing(escg_dev* h, double* ms, int64_t* launches);
 
-/* Kernel actually selected (ESCG_KERNEL_TILE / ESCG_KERNEL_BLOCK) and its launch geometry. */
+/* Kernel actually selected (ESCG_KERNEL_TILE / _BLOCK / _RING) and its launch geometry. */
 ESCG_API int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t* threads, int32_t* smem_bytes);
 
 /* Draw format chosen for this engine: 0 WIDE (32-bit attempt words), 1 NARROW (16-bit words, one
@@ -151,8 +154,9 @@ ESCG_API int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas,
  * bit-sliced block kernel) — DESIGN.md §RNG; the oracle needs it to replay the schedule. */
 ESCG_API int escg_dev_draw_format(escg_dev* h, int32_t* narrow);
 
-/* Block kernel mode: MCS per chunk (temporal blocking; 1 for the tile kernel) and whether a run
- * executes as one persistent cooperative launch (1) or one launch per chunk (0). */
+/* Block kernel mode: MCS per chunk (temporal blocking; 1 for the tile kernel; 0 for the ring kernel,
+ * whose launch covers the whole advance/run) and whether a run executes as one persistent
+ * cooperative launch (1) or one launch per chunk (0). */
 ESCG_API int escg_dev_block_mode(escg_dev* h, int32_t* kmcs, int32_t* persistent);
 
 /* Row-band sharding of one lattice.  Band `band` of `n_bands` (rows split at

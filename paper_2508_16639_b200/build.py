@@ -12,8 +12,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libescg_b200.so")
-SOURCES = ["kernels.cu", "slice.cu", "engine.cpp"]
-HEADERS = ["crs.cuh", "launch.h", "record.cuh"]
+SOURCES = ["kernels.cu", "slice.cu", "ring.cu", "engine.cpp"]
+HEADERS = ["crs.cuh", "launch.h", "record.cuh", "slice_common.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v",

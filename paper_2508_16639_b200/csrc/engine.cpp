@@ -191,6 +191,9 @@ struct escg_dev {
     int qcap = 0;    // SLICED: deferred-tile queue capacity override (tests)
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
+    // SLICED single lattices on the persistent ring kernel (ring.cu): bands, shared memory, mailboxes
+    bool ring = false;
+    int ring_nb = 0, ring_smem = 0, ring_mbs = 0;
     int bh_max = 0, bw_max = 0;
     int seam_np = 0;  // block kernel on a periodic lattice with seams: colour phases per MCS (4, 6, 9)
     int phase_table = 0;  // block kernel: per-launch phase-geometry table (few items per thread)
@@ -221,6 +224,8 @@ struct escg_dev {
     DevBuf<int32_t> d_cur;
     DevBuf<unsigned long long> d_acc3;
     DevBuf<int32_t> d_i32;
+    DevBuf<unsigned long long> d_mbox;
+    DevBuf<unsigned int> d_decided;
     int64_t trace_cap = 0;
     bool traced = false;
     double last_ms = 0.0;
@@ -540,6 +545,36 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     return launches;
 }
 
+// Ring path: the whole advance (record = 0; final lattice in plane buffer 1) or run (records at
+// t0 + k*interval and at the limit; record k in plane buffer k & 1, named by cur) in one launch.
+void enqueue_ring(escg_dev* h, int64_t t0, int64_t t1, int record, const escgd::RunArgs& run) {
+    escgd::RingArgs a{};
+    a.pin = h->pl[0].p;
+    a.pbuf[0] = h->pl[0].p;
+    a.pbuf[1] = h->pl[1].p;
+    a.seeds = h->d_seeds.p;
+    a.rule = rule_args(h);
+    a.run = run;
+    a.H = h->H;
+    a.L = h->L;
+    a.S = h->S;
+    a.npl = h->npl;
+    a.K = h->K;
+    a.mcs0 = t0;
+    a.mcs_end = t1;
+    a.record = record;
+    a.mbox = h->d_mbox.p;
+    a.mbs = h->ring_mbs;
+    a.decided = h->d_decided.p;
+    a.acc = h->d_acc.p;
+    a.ticket = h->d_ticket.p;
+    a.smem_bytes = h->ring_smem;
+    a.qcap = h->qcap;
+    CK(cudaMemsetAsync(h->d_mbox.p, 0, sizeof(unsigned long long) * h->d_mbox.n, h->stream));
+    CK(cudaMemsetAsync(h->d_decided.p, 0, sizeof(unsigned int), h->stream));
+    CK(escgd::launch_ring(a, h->ring_nb, h->stream));
+}
+
 escgd::PersistArgs persist_args(escg_dev* h, const escgd::RunArgs& run) {
     escgd::PersistArgs pa{};
     escgd::BlockArgs& a = pa.b;
@@ -674,6 +709,23 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         } else {
             CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
             ++launches;
+        }
+        if (h->ring) {
+            // one persistent launch for the whole run (records and stop decisions on device)
+            if (limit > t0) {
+                enqueue_ring(h, t0, limit, 1, run);
+                ++launches;
+            }
+            CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, h->d_cur.p, 0, h->lat[0].p, h->H, h->L, h->npl,
+                                         h->nrep, h->stream));
+            ++launches;
+            timed_end(h, launches);
+            CK(cudaGetLastError());
+            std::vector<int32_t> st(h->nrep);
+            CK(cudaMemcpy(h->mcs.data(), h->d_mcs.p, sizeof(int64_t) * h->nrep, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(st.data(), h->d_status.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost));
+            if (status_out) std::memcpy(status_out, st.data(), sizeof(int32_t) * h->nrep);
+            return;
         }
         // Poll the device status every few chunks so a stasis/stop does not leave thousands of
         // no-op launches queued; the poll lags one chunk behind the enqueue front.
@@ -900,7 +952,8 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             if (const char* tv = std::getenv("ESCG_TILE_THREADS"))
                 tile_threads = std::max(32, std::min(cap, (std::atoi(tv) + 31) / 32 * 32));
         }
-        int choice = kernel;
+        if (kernel < ESCG_KERNEL_AUTO || kernel > ESCG_KERNEL_RING) config_error("unknown kernel selection");
+        int choice = kernel == ESCG_KERNEL_RING ? ESCG_KERNEL_BLOCK : kernel;
         if (choice == ESCG_KERNEL_AUTO) {
             // one CTA per replica (tile) wins only when the replicas fill the device: at least one
             // per SM and a quarter of the tile kernel's concurrent CTAs; fewer lattices run faster
@@ -944,6 +997,10 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                             h->S <= 7 && lead >= 6;
             bool use = ok && lead >= 8;
             if (const char* f = std::getenv("ESCG_DRAW_FORMAT")) use = ok && std::strcmp(f, "sliced") == 0;
+            if (kernel == ESCG_KERNEL_RING) {
+                if (!ok) config_error("the ring kernel needs the bit-sliced draw format (periodic von Neumann, L % 128 == 0, S <= 7, P(migration) >= 0.98)");
+                use = true;
+            }
             if (use) {
                 h->narrow = 2;
                 h->K = std::min(lead, escgd::kSliceMaxK) & ~1;
@@ -1003,6 +1060,32 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 h->persist = h->nby * h->nbx * n_replicas <= cap;
             }
             if (h->persist) h->d_acc3.alloc(static_cast<size_t>(3) * n_replicas * h->S1);
+            // ring kernel (ring.cu): single periodic bit-sliced lattices whose rows fit one warp
+            // (L/128 <= 32 groups), one band of >= 8 rows per SM.  AUTO takes it from L >= 1024
+            // (8 busy lanes per warp); ESCG_KERNEL_RING forces it (tests: any L/128 <= 32).
+            if (h->narrow == 2 && !bs && n_replicas == 1 &&
+                (kernel == ESCG_KERNEL_RING ||
+                 (kernel == ESCG_KERNEL_AUTO && !(std::getenv("ESCG_RING") && std::getenv("ESCG_RING")[0] == '0')))) {
+                const int GL = h->L / 128;
+                int nb = std::min(prop.multiProcessorCount, h->H / 8);
+                if (const char* nv = std::getenv("ESCG_RING_NB")) nb = std::max(2, std::min(nb, std::atoi(nv)));
+                int coop = 0;
+                CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+                const int rsmem = nb >= 2 ? escgd::ring_smem_bytes(h->H, h->L, h->npl, nb) : 0;
+                const bool ok = coop && nb >= 2 && GL <= 32 && (kernel == ESCG_KERNEL_RING || GL >= 8) &&
+                                rsmem <= std::min(smem_cap, 200 * 1024) &&
+                                nb <= escgd::ring_capacity(h->npl, rsmem, device);
+                if (ok) {
+                    h->ring = true;
+                    h->ring_nb = nb;
+                    h->ring_smem = rsmem;
+                    h->ring_mbs = 2 + 3 * h->npl * GL * 4;
+                    h->d_mbox.alloc(static_cast<size_t>(nb) * 4 * h->ring_mbs);
+                    h->d_decided.alloc(1);
+                } else if (kernel == ESCG_KERNEL_RING) {
+                    config_error("lattice not eligible for the ring kernel (L/128 <= 32, H >= 16, co-resident bands)");
+                }
+            }
             h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
             h->d_ticket.alloc(n_replicas);
         }
@@ -1170,7 +1253,13 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
             const int64_t t0 = h->mcs[0];
             int64_t launch_no = 0;
             timed_begin(h);
-            if (h->narrow == 2 && n_mcs > 0) {
+            if (h->ring && n_mcs > 0) {
+                CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+                enqueue_ring(h, t0, t0 + n_mcs, 0, run);  // final lattice in plane buffer 1
+                CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, 1, h->lat[0].p, h->H, h->L, h->npl,
+                                             h->nrep, h->stream));
+                launches = 3;
+            } else if (h->narrow == 2 && n_mcs > 0) {
                 CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
                 launches = 1 + enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
                 CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, static_cast<int>(launch_no & 1),
@@ -1280,18 +1369,18 @@ int escg_dev_last_timing(escg_dev* h, double* ms, int64_t* launches) {
 int escg_dev_describe(escg_dev* h, int32_t* kernel, int32_t* grid_ctas, int32_t* threads, int32_t* smem_bytes) {
     return guarded([&] {
         if (!h) config_error("null handle");
-        if (kernel) *kernel = h->kernel;
-        if (grid_ctas) *grid_ctas = h->kernel == ESCG_KERNEL_TILE ? h->nrep : h->nby * h->nbx * h->nrep;
-        if (threads) *threads = h->threads;
-        if (smem_bytes) *smem_bytes = h->smem;
+        if (kernel) *kernel = h->ring ? ESCG_KERNEL_RING : h->kernel;
+        if (grid_ctas) *grid_ctas = h->ring ? h->ring_nb : (h->kernel == ESCG_KERNEL_TILE ? h->nrep : h->nby * h->nbx * h->nrep);
+        if (threads) *threads = h->ring ? escgd::kRingThreads : h->threads;
+        if (smem_bytes) *smem_bytes = h->ring ? h->ring_smem : h->smem;
     });
 }
 
 int escg_dev_block_mode(escg_dev* h, int32_t* kmcs, int32_t* persistent) {
     return guarded([&] {
         if (!h) config_error("null argument");
-        if (kmcs) *kmcs = h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1;
-        if (persistent) *persistent = (h->kernel == ESCG_KERNEL_BLOCK && h->persist) ? 1 : 0;
+        if (kmcs) *kmcs = h->ring ? 0 : (h->kernel == ESCG_KERNEL_BLOCK ? h->kmcs : 1);
+        if (persistent) *persistent = (h->kernel == ESCG_KERNEL_BLOCK && (h->persist || h->ring)) ? 1 : 0;
     });
 }
 

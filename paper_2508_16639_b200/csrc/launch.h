@@ -165,6 +165,30 @@ int slice_kernel_registers(int npl, int lpi);
 cudaError_t launch_to_planes(const uint8_t* lat, uint32_t* pl, int H, int L, int npl, int nrep, cudaStream_t s);
 cudaError_t launch_from_planes(const uint32_t* pl0, const uint32_t* pl1, const int32_t* cur, int buf, uint8_t* lat,
                                int H, int L, int npl, int nrep, cudaStream_t s);
+// Persistent bit-sliced ring kernel (ring.cu): one co-resident CTA per row band of
+// full-width rows; colour phases exchange boundary rows with the two neighbour bands through L2
+// mailboxes (data words tagged with the phase), so no area is recomputed.
+constexpr int kRingThreads = 256;
+struct RingArgs {
+    const uint32_t* pin;      // input planes [H][NPL][L/128][4]
+    uint32_t* pbuf[2];        // snapshots: record k of the launch -> pbuf[k & 1]; advance -> pbuf[1]
+    const uint64_t* seeds;
+    RuleArgs rule;
+    RunArgs run;              // replica 0; run.interval = record cadence
+    int H, L, S, npl, K;
+    int64_t mcs0, mcs_end;    // MCS [mcs0, mcs_end)
+    int record;               // 1: density records at mcs0 + k*interval and at mcs_end; 0: advance
+    unsigned long long* mbox; // [nb][dir][parity][mbs] tagged words (zeroed before every launch)
+    int mbs;                  // words per mailbox: 2 header + 3 rows x NPL x L/128 x 4
+    unsigned int* decided;    // records decided in this launch (zeroed before the launch)
+    unsigned long long* acc;  // [S+1] record accumulators (zero between records)
+    unsigned int* ticket;
+    int smem_bytes;
+    int qcap;                 // > 0: per-warp deferred-tile queue capacity override (tests)
+};
+cudaError_t launch_ring(const RingArgs& a, int nb, cudaStream_t s);
+int ring_smem_bytes(int H, int L, int npl, int nb);
+int ring_capacity(int npl, int smem_bytes, int device);  // co-resident CTAs (cooperative launch)
 cudaError_t launch_u8_to_i32(const uint8_t* src, int32_t* dst, int64_t n, cudaStream_t s);
 cudaError_t launch_i32_to_u8(const int32_t* src, uint8_t* dst, int64_t n, int S, int* bad, cudaStream_t s);
 int tile_smem_bytes(int H, int L, int S, int* pitch);

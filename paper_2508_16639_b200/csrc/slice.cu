@@ -33,42 +33,10 @@
 #include "crs.cuh"
 #include "launch.h"
 #include "record.cuh"
+#include "slice_common.cuh"
 
 namespace escgd {
 namespace {
-
-#ifdef ESCG_DIAG_SLICE
-// diagnostic builds only (tools/slice_diag.py): clock64 stamps of CTA 0..3, warps 0..15, phases 0..7
-__device__ long long g_sdiag[4][16][8][8];
-#define SDIAG(ph, ev)                                                                                  \
-    do {                                                                                              \
-        const int cta_ = blockIdx.x + gridDim.x * blockIdx.y;                                         \
-        if (cta_ < 4 && (threadIdx.x & 31) == 0 && (threadIdx.x >> 5) < 16 && (ph) < 8)                \
-            g_sdiag[cta_][threadIdx.x >> 5][ph][ev] = clock64();                                      \
-    } while (0)
-#else
-#define SDIAG(ph, ev)
-#endif
-constexpr uint32_t kDomSlice = 4, kDomSliceRef = 5;
-constexpr int kMaxSliceSpecies = 7;  // NPL <= 3 bit planes
-constexpr unsigned kSliceQueue = 512;  // deferred tiles per phase replayed CTA-wide
-constexpr uint32_t kFull = 0xffffffffu;
-
-__device__ __forceinline__ uint4 lds128(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
-// ordered shared load (the replay's next attempt reads what the previous one's red.xor wrote)
-__device__ __forceinline__ uint32_t lds32o(uint32_t a) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
-    return v;
-}
-__device__ __forceinline__ void sts128(uint32_t* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
-
-// Shared-memory words per window row: NPL planes x Gw groups x 4 quads, padded to 4 (mod 8) words
-// so that the two tile rows of a quarter-warp (Gw = 4) hit disjoint bank quads.
-__host__ __device__ __forceinline__ int row_words(int npl, int gw) {
-    const int base = npl * gw * 4;
-    return (base & 7) == 0 ? base + 4 : base;
-}
 
 // Footprint word at column offset DX (-1..2) of a row from the group's quad words: column
 // anchor + DX = 4b + t with t = XR + DX, i.e. quad t & 3 at bit b + (t >> 2).  The neighbouring
@@ -119,80 +87,6 @@ struct SliceCtx {
     unsigned* qn;         // its fill count
     unsigned qcap;        // its capacity (<= kSliceQueue; smaller in tests of the overflow path)
 };
-
-// Exact replay of one tile whose attempts left the bit-parallel pass (engine.hpp:108-141), on the
-// tile's 12 footprint cells held as 3-bit fields of one register: the cells are read once, the four
-// attempts run branch-free in registers, and the changed bits are written back with shared-memory
-// XOR reductions (neighbouring lanes share the boundary words).  sw0 = shared address of the
-// window; code: 4 choice bits per attempt (cell row, cell column, direction) in nibble a,
-// undecided flag of attempt a in bit 16 + a.  Footprint positions: 0 (0,1) 1 (0,2) 2 (1,0) 3 (1,1)
-// 4 (1,2) 5 (1,3) 6 (2,0) 7 (2,1) 8 (2,2) 9 (2,3) 10 (3,1) 11 (3,2) as (row - w + 1, col - acol + 1).
-template <int NPL>
-__device__ __forceinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code,
-                                             uint32_t item, int l, uint32_t c1, uint32_t c2r, uint32_t s32, uint32_t xm,
-                                             uint32_t xi, uint32_t TK, uint32_t sT, int S1, int qd = 8) {
-    constexpr int kRow[12] = {0, 0, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3};
-    constexpr int kCol[12] = {1, 2, 0, 1, 2, 3, 0, 1, 2, 3, 1, 2};
-    constexpr uint32_t kCellPos = 0x8473u;               // position of cell (Y, X): nibble Y | X << 1
-    constexpr uint64_t kNbrPos = 0x95847362b8a74130ull;  // neighbour position: nibble Y | X << 1 | dir << 2
-    if (acol < 1 || acol + 2 >= 128 * Gw) return;  // window edge: margin cells, never stored
-#ifdef ESCG_DIAG_REPLAY_NOPHILOX
-    const uint4 rf = make_uint4(item ^ c1, c2r + l, s32, item);
-#else
-    const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);
-#endif
-    const uint32_t PS = static_cast<uint32_t>(Gw) * 16u;  // plane stride (bytes)
-    uint32_t addr[12], bit[12];
-    uint64_t cells = 0;
-#pragma unroll
-    for (int k = 0; k < 12; ++k) {
-        const int row = w - 1 + kRow[k], col = acol - 1 + kCol[k];
-        addr[k] = sw0 + 4u * static_cast<uint32_t>(row * RP + (col >> 7) * 4 + (col & 3));
-        bit[k] = (static_cast<uint32_t>(col) >> 2) & 31u;
-        uint32_t v = 0;
-#pragma unroll
-        for (int p = 0; p < NPL; ++p) v |= ((lds32o(addr[k] + p * PS) >> bit[k]) & 1u) << p;
-        cells |= static_cast<uint64_t>(v) << (3 * k);
-    }
-#ifdef ESCG_DIAG_SLICE
-    if ((cells + rf.x) != 1u) SDIAG(qd, 6);
-#endif
-    const uint64_t cells0 = cells;
-    const uint32_t rw[4] = {rf.x, rf.y, rf.z, rf.w};
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const uint32_t cb = (code >> (4 * a)) & 15u;
-        const uint32_t ps = (kCellPos >> (4 * (cb & 3u))) & 15u, pn = static_cast<uint32_t>(kNbrPos >> (4 * cb)) & 15u;
-        const uint32_t s = static_cast<uint32_t>(cells >> (3 * ps)) & 7u, n = static_cast<uint32_t>(cells >> (3 * pn)) & 7u;
-        // the rule (engine.hpp:111-140) with selects; a decided attempt is a certain migration
-        const bool und = (code >> (16 + a)) & 1u;
-        const uint32_t x = TK | (rw[a] & ~TK);
-        const bool mig = !und || x < xm, rep = und && x >= xi;
-        const bool inter = !mig && !rep && s != 0u && n != 0u && s != n;
-        const uint32_t t1 = lds32_if(inter, sT + 4u * (s * S1 + n), 0u);
-        const uint32_t t2 = lds32_if(inter, sT + 4u * (n * S1 + s), 0u);
-        const bool kn = inter && x < t1, ks = inter && !(x < t1) && x < t2;
-        const bool r1 = rep && n == 0u, r2 = rep && n != 0u && s == 0u;
-        const uint32_t ns = mig ? n : (ks ? 0u : (r2 ? n : s));
-        const uint32_t nn = mig ? s : (kn ? 0u : (r1 ? s : n));
-        cells = (cells & ~((7ull << (3 * ps)) | (7ull << (3 * pn)))) | (static_cast<uint64_t>(ns) << (3 * ps)) |
-                (static_cast<uint64_t>(nn) << (3 * pn));
-    }
-    const uint64_t delta = cells ^ cells0;
-#ifdef ESCG_DIAG_SLICE
-    if (delta != 1u) SDIAG(qd, 5);
-#endif
-#ifndef ESCG_DIAG_REPLAY_NOATOM
-#pragma unroll
-    for (int k = 0; k < 12; ++k)
-#pragma unroll
-        for (int p = 0; p < NPL; ++p)
-            if ((delta >> (3 * k + p)) & 1u)
-                asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[k] + p * PS), "r"(1u << bit[k]) : "memory");
-#else
-    if (delta == 0x123456789ull) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[0]), "r"(1u) : "memory");
-#endif
-}
 
 // Out-of-line copy for the in-place overflow path inside the (per-residue) phase bodies.
 template <int NPL>
@@ -375,88 +269,6 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
                 slice_replay_ool<NPL>(C.sw0, C.RP, C.Gw, w, acol, code, item, l, c1, c2r, C.s32, C.xm, C.xi, C.TK, C.sT,
                                   C.S1);
             }
-        }
-    }
-}
-
-// Group replay: the 8 lanes of group (lane >> 3) replay one tile together.  Lane j reads and writes
-// footprint positions j and j + 8 (the 24 shared-memory reads and up to 24 XOR reductions of a
-// tile are spread over the group); the packed cells are OR-combined with shuffles, and every lane
-// of the group runs the four attempts on the same register copy (the exact rule, branch-free).
-template <int NPL>
-__device__ __forceinline__ void slice_replay_group(uint32_t sw0, int RP, int Gw, int w, int acol, uint32_t code,
-                                                   uint32_t item, int l, uint32_t c1, uint32_t c2r, uint32_t s32,
-                                                   uint32_t xm, uint32_t xi, uint32_t TK, uint32_t sT, int S1,
-                                                   bool active) {
-    constexpr int CB = NPL == 2 ? 2 : 3;  // bits per packed cell
-    using Pack = typename std::conditional<NPL == 2, uint32_t, uint64_t>::type;
-    constexpr uint32_t kCellPos = 0x8473u;
-    constexpr uint64_t kNbrPos = 0x95847362b8a74130ull;
-    constexpr uint32_t kRow = 0xFAA550u;  // 2-bit row offset + 1 of position k: 0 0 1 1 1 1 2 2 2 2 3 3
-    constexpr uint32_t kCol = 0x9E4E49u;  // 2-bit column offset + 1 of position k: 1 2 0 1 2 3 0 1 2 3 1 2
-    const int j = threadIdx.x & 7;
-    const bool ok = active && acol >= 1 && acol + 2 < 128 * Gw;  // window edge: margin cells, skipped
-    const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), s32);  // overlaps the reads
-    const uint32_t PS = static_cast<uint32_t>(Gw) * 16u;
-    uint32_t addr[2] = {0u, 0u}, bit[2] = {0u, 0u};
-    Pack part = 0;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        const int k = j + 8 * t;
-        if (ok && k < 12) {
-            const int rr = static_cast<int>((kRow >> (2 * k)) & 3u);
-            const int cc = static_cast<int>((kCol >> (2 * k)) & 3u);
-            const int row = w - 1 + rr, col = acol - 1 + cc;
-            addr[t] = sw0 + 4u * static_cast<uint32_t>(row * RP + (col >> 7) * 4 + (col & 3));
-            bit[t] = (static_cast<uint32_t>(col) >> 2) & 31u;
-            uint32_t v = 0;
-#pragma unroll
-            for (int p = 0; p < NPL; ++p) v |= ((lds32(addr[t] + p * PS) >> bit[t]) & 1u) << p;
-            part |= static_cast<Pack>(v) << (CB * k);
-        }
-    }
-    Pack cells = part;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-        if constexpr (NPL == 2) {
-            cells |= __shfl_xor_sync(kFull, cells, o);
-        } else {
-            const uint32_t lo = __shfl_xor_sync(kFull, static_cast<uint32_t>(cells), o);
-            const uint32_t hi = __shfl_xor_sync(kFull, static_cast<uint32_t>(cells >> 32), o);
-            cells |= (static_cast<uint64_t>(hi) << 32) | lo;
-        }
-    }
-    if (!ok) return;
-    const Pack cells0 = cells;
-    const uint32_t rw[4] = {rf.x, rf.y, rf.z, rf.w};
-    constexpr Pack M = (static_cast<Pack>(1) << CB) - 1;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const uint32_t cb = (code >> (4 * a)) & 15u;
-        const uint32_t ps = (kCellPos >> (4 * (cb & 3u))) & 15u, pn = static_cast<uint32_t>(kNbrPos >> (4 * cb)) & 15u;
-        const uint32_t s = static_cast<uint32_t>(cells >> (CB * ps)) & M, n = static_cast<uint32_t>(cells >> (CB * pn)) & M;
-        const bool und = (code >> (16 + a)) & 1u;
-        const uint32_t x = TK | (rw[a] & ~TK);
-        const bool mig = !und || x < xm, rep = und && x >= xi;
-        const bool inter = !mig && !rep && s != 0u && n != 0u && s != n;
-        const uint32_t t1 = lds32_if(inter, sT + 4u * (s * S1 + n), 0u);
-        const uint32_t t2 = lds32_if(inter, sT + 4u * (n * S1 + s), 0u);
-        const bool kn = inter && x < t1, ks = inter && !(x < t1) && x < t2;
-        const bool r1 = rep && n == 0u, r2 = rep && n != 0u && s == 0u;
-        const uint32_t ns = mig ? n : (ks ? 0u : (r2 ? n : s));
-        const uint32_t nn = mig ? s : (kn ? 0u : (r1 ? s : n));
-        cells = (cells & ~((M << (CB * ps)) | (M << (CB * pn)))) | (static_cast<Pack>(ns) << (CB * ps)) |
-                (static_cast<Pack>(nn) << (CB * pn));
-    }
-    const Pack delta = cells ^ cells0;
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-        const int k = j + 8 * t;
-        if (k < 12) {
-#pragma unroll
-            for (int p = 0; p < NPL; ++p)
-                if ((delta >> (CB * k + p)) & 1u)
-                    asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(addr[t] + p * PS), "r"(1u << bit[t]) : "memory");
         }
     }
 }

@@ -323,7 +323,7 @@ class DeviceEngine:
         self.model = model
         self.n_replicas = int(n_replicas)
         self.S = int(model.size)
-        kern = {"auto": 0, "tile": 1, "block": 2}[kernel]
+        kern = {"auto": 0, "tile": 1, "block": 2, "ring": 3}[kernel]
         seeds_arr = None
         if seeds is not None:
             seeds_arr = np.ascontiguousarray([int(s) & 0xFFFFFFFFFFFFFFFF for s in seeds], np.uint64)
@@ -437,7 +437,7 @@ class DeviceEngine:
         kernel, ctas, threads, smem = (v.value for v in vals)
         k, pers = C.c_int32(0), C.c_int32(0)
         check(lib().escg_dev_block_mode(self._h, C.byref(k), C.byref(pers)))
-        return dict(kernel={1: "tile", 2: "block"}[kernel], ctas=ctas, threads=threads, smem_bytes=smem,
+        return dict(kernel={1: "tile", 2: "block", 3: "ring"}[kernel], ctas=ctas, threads=threads, smem_bytes=smem,
                     draw_format=self.draw_format(), kmcs=k.value, persistent=bool(pers.value))
 
 
