@@ -29,11 +29,12 @@ with e.DeviceEngine(p, e.make_circulant(3, [1]), kernel="ring") as eng:
     fn(None, 1)
     eng.advance(300)
     ms, _ = eng.last_timing()
-    buf = np.zeros(160 * 32 * 8 * 8 + 160 * 32, np.int64)
+    buf = np.zeros(160 * 32 * 8 * 8 + 160 * 32 + 160 * 32 * 4, np.int64)
     fn(buf.ctypes.data, 0)
     d_ = eng.describe()
 print(d_, "advance(300): %.3f ms = %.2f us/MCS" % (ms, ms * 1e3 / 300))
-polls = buf[160 * 32 * 8 * 8:].view(np.int32).reshape(160, 32, 2)
+polls = buf[160 * 32 * 8 * 8:160 * 32 * 8 * 8 + 160 * 32].view(np.int32).reshape(160, 32, 2)
+gt = buf[160 * 32 * 8 * 8 + 160 * 32:].reshape(160, 32, 4)
 d = buf[:160 * 32 * 8 * 8].reshape(160, 32, 8, 8)
 nb = d_["ctas"]
 d = d[:nb]
@@ -60,3 +61,16 @@ for label, ws in (("warp0 (top)", [0]), ("warp1 (bottom)", [1]), ("interior", [2
     print("%-15s start %6.0f | " % (label, np.median(st)) +
           " | ".join("%s %6.0f" % (n, np.median(s[:, i])) for i, n in enumerate(names)) +
           " | sum %6.0f (p90 %6.0f)" % (np.median(s.sum(1)), np.percentile(s.sum(1), 90)))
+
+gt = gt[:nb].astype(np.float64)
+# top import of band c at phase q waits for band c-1's bottom publish of phase q
+lat_top = gt[:, :, 2] - np.roll(gt[:, :, 1], 1, axis=0)
+lat_bot = gt[:, :, 3] - np.roll(gt[:, :, 0], -1, axis=0)
+ok = (gt[:, :, 2] > 0) & (np.roll(gt[:, :, 1], 1, axis=0) > 0)
+lt = np.concatenate([lat_top[ok], lat_bot[ok]])
+print("publish -> import done (ns): median %.0f  p10 %.0f  p90 %.0f" % (np.median(lt), np.percentile(lt, 10), np.percentile(lt, 90)))
+for w, nm in ((6, "producer top"), (7, "producer bottom")):
+    x = d[:, :, w, :].astype(np.float64)
+    ok = x[..., 0] > 0
+    print("%-15s draws %6.0f | import %6.0f | phase period %6.0f" % (nm, np.median((x[..., 1] - x[..., 0])[ok]),
+          np.median((x[..., 2] - x[..., 1])[ok]), np.median(np.diff(x[..., 0], axis=1)[ok[:, 1:] & ok[:, :-1]])))
