@@ -1,5 +1,7 @@
 """bench.py — site-update attempts/s of the ESCG Monte Carlo step path at L=3200 (BASELINE.json).
 
+    python bench.py --config C1|C2|C5 prints the same line for the other single-lattice BASELINE configs.
+
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 Workload (BASELINE.json configs[2], the headline): RPS (C(3,{1})) on a 3200x3200 periodic von-Neumann
@@ -26,27 +28,49 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-L = 3200
-M = 1e-4
-P0 = 0.1
-NUM_RANDOMS = 100000000
-MCS_PER_STEP = 900
 METRIC = "site-update attempts/sec and MCS/sec at L=3200 (1/2/4/8 B200) vs CPU ref"
 UNIT = "attempts/s"
-# BASELINE.md / PAPER.md:1366: CUDA-MS (maxStep) L=3200 on RTX A2000, 4173.50 s for 1e5 MCS
-PUBLISHED_ATTEMPTS_PER_S = 3200 * 3200 * 1e5 / 4173.50
+
+# BASELINE.json configs.  C3 is the headline the driver runs; --config C1|C2|C5 prints the
+# same line for the other single-lattice configurations (C4 is an ensemble: tests/test_gpu_stats2.py).
+# published: the paper's CUDA-MS (maxStep) wall time for 1e5 MCS on an RTX A2000 at that L
+# (BASELINE.md §1), None where the paper has no number for the config.
+CONFIGS = {
+    "C3": dict(L=3200, S=3, model="rps", M=1e-4, p0=0.1, num_randoms=100000000, mcs_per_step=900,
+               cpu_maxstep_mcs=200, cpu_serial_mcs=6, ref_step_mcs=10, published=4173.50,
+               desc="RPS C(3,{1}) L=3200 M=1e-4 p0=0.1 VN4 periodic, MaxStep record cadence (9 MCS)",
+               published_ref="PAPER.md:1366 CUDA-MS L=3200 RTX A2000: 4173.50 s / 1e5 MCS"),
+    "C1": dict(L=200, S=3, model="rps", M=1e-4, p0=0.1, num_randoms=100000000, mcs_per_step=2500,
+               cpu_maxstep_mcs=5000, cpu_serial_mcs=2500, ref_step_mcs=500, published=6.93,
+               desc="RPS C(3,{1}) L=200 M=1e-4 p0=0.1 VN4 periodic (Reichenbach-Mobilia-Frey), one lattice, "
+                    "MaxStep record cadence (2500 MCS)",
+               published_ref="PAPER.md:1358 CUDA-MS L=200 RTX A2000: 6.93 s / 1e5 MCS"),
+    "C2": dict(L=1000, S=5, model="rpsls", M=3e-5, p0=0.0, num_randoms=100000000, mcs_per_step=500,
+               cpu_maxstep_mcs=200, cpu_serial_mcs=50, ref_step_mcs=20, published=None,
+               desc="RPSLS C(5,{1,2}) L=1000 M=3e-5 p0=0 VN4 periodic, one lattice, MaxStep record cadence (100 MCS)",
+               published_ref=None),
+    "C5": dict(L=16384, S=3, model="rps", M=1e-4, p0=0.1, num_randoms=5 * 16384 * 16384, mcs_per_step=20,
+               cpu_maxstep_mcs=2, cpu_serial_mcs=None, ref_step_mcs=1, published=None,
+               desc="RPS C(3,{1}) L=16384 M=1e-4 p0=0.1 VN4 periodic (268M cells), MaxStep record cadence with "
+                    "numRandoms = 5N (5 MCS)",
+               published_ref=None),
+}
 
 
-def workload_config(extra=None):
-    cfg = {"workload": "RPS C(3,{1}) L=3200 M=1e-4 p0=0.1 VN4 periodic, MaxStep record cadence (9 MCS), "
-                       "%d MCS per step" % MCS_PER_STEP,
-           "L": L, "species": 3, "mobility": M, "empty_prob": P0, "num_randoms": NUM_RANDOMS,
-           "mcs_per_step": MCS_PER_STEP, "l2": "flushed between timed steps (256 MiB device write)",
-           "vs_baseline_ref": "PAPER.md:1366 CUDA-MS L=3200 RTX A2000: 4173.50 s / 1e5 MCS = %.3g attempts/s"
-                              % PUBLISHED_ATTEMPTS_PER_S}
+def published_rate(cfg):
+    """attempts/s of the paper's CUDA-MS number for this L (None if the paper has none)."""
+    return cfg["L"] * cfg["L"] * 1e5 / cfg["published"] if cfg["published"] else None
+
+
+def workload_config(cfg, extra=None):
+    out = {"workload": "%s, %d MCS per step" % (cfg["desc"], cfg["mcs_per_step"]), "L": cfg["L"],
+           "species": cfg["S"], "mobility": cfg["M"], "empty_prob": cfg["p0"], "num_randoms": cfg["num_randoms"],
+           "mcs_per_step": cfg["mcs_per_step"], "l2": "flushed between timed steps (256 MiB device write)"}
+    if cfg["published_ref"]:
+        out["vs_baseline_ref"] = "%s = %.3g attempts/s" % (cfg["published_ref"], published_rate(cfg))
     if extra:
-        cfg.update(extra)
-    return cfg
+        out.update(extra)
+    return out
 
 
 def dist_env():
@@ -60,38 +84,44 @@ def dist_env():
 # CPU reference (oracle/_ref = unmodified reference engine)
 # ---------------------------------------------------------------------------------------------
 
-def reference_sample(mcs, mode=2, workers=None, seed=1):
-    """simulate(params, C(3,{1}), mode) on the host; returns (attempts/s, wall s of the timed window,
-    workers).  Window: first on_record → return, so init and burn-in are excluded."""
+def reference_sample(cfg, mcs, mode=2, workers=None, seed=1):
+    """simulate(params, model, mode) of the unmodified reference on the host; returns (attempts/s,
+    wall s of the timed window, workers).  Window: first on_record -> return, so init and
+    burn-in are excluded."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from pyoracle import Reference
 
     r = Reference()
     workers = workers or os.cpu_count()
-    dom = r.circulant(3, [1])
+    L = cfg["L"]
+    dom = r.circulant(3, [1]) if cfg["model"] == "rps" else r.circulant(5, [1, 2])
     num_randoms = L * L * 5  # 5 MCS per batch (≈ the paper's optimum, PAPER.md:1321), double-buffered
-    res = r.simulate(L, L, dom, M, P0, mcs, seed, mode=mode, workers=workers if mode else 1,
+    res = r.simulate(L, L, dom, cfg["M"], cfg["p0"], mcs, seed, mode=mode, workers=workers if mode else 1,
                      num_randoms=num_randoms, cap=mcs + 2, want_cells=False)
     elapsed = res["elapsed_s"]
     return L * L * mcs / elapsed, elapsed, (workers if mode else 1)
 
 
-def cpu_baseline():
-    # ~10 s wall on 16 host cores (~2e8 attempts/s): a bounded sample of the L=3200 workload
-    v, el, w = reference_sample(mcs=200, mode=2)
+def cpu_baseline(cfg):
+    # run_max_step on all host cores over a bounded window of the same workload
+    v, el, w = reference_sample(cfg, mcs=cfg["cpu_maxstep_mcs"], mode=2)
     out = {"value": v, "unit": UNIT, "cores": w, "kind": "reference",
-           "sample": "reference run_max_step (ThreadPool(%d)), RPS L=3200 M=1e-4 p0=0.1, 200 MCS window "
-                     "from the first density record (%.1f s wall)" % (w, el)}
-    # SURVEY §8d's single-core comparison: run_serial (EngineMode::Serial) pinned to one core, ~8 s
-    aff = os.sched_getaffinity(0)
-    try:
-        os.sched_setaffinity(0, {min(aff)})
-        sv, sel, _ = reference_sample(mcs=6, mode=0)
-    finally:
-        os.sched_setaffinity(0, aff)
-    out["serial"] = {"value": sv, "unit": UNIT, "cores": 1, "kind": "reference",
-                     "sample": "reference run_serial pinned to core %d, RPS L=3200 M=1e-4 p0=0.1, 6 MCS window "
-                               "(%.1f s wall)" % (min(aff), sel)}
+           "sample": "reference run_max_step (ThreadPool(%d)), %s, %d MCS window from the first density record "
+                     "(%.1f s wall)" % (w, cfg["desc"].split(",")[0], cfg["cpu_maxstep_mcs"], el)}
+    # SURVEY §8d's single-core comparison: run_serial (EngineMode::Serial) pinned to one core
+    if cfg["cpu_serial_mcs"]:
+        aff = os.sched_getaffinity(0)
+        try:
+            os.sched_setaffinity(0, {min(aff)})
+            sv, sel, _ = reference_sample(cfg, mcs=cfg["cpu_serial_mcs"], mode=0)
+        finally:
+            os.sched_setaffinity(0, aff)
+        out["serial"] = {"value": sv, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": "reference run_serial pinned to core %d, %d MCS window (%.1f s wall)"
+                                   % (min(aff), cfg["cpu_serial_mcs"], sel)}
+    else:
+        out["serial"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": "not run: the single-core reference needs ~70 s per MCS at this size (SURVEY §8d)"}
     return out
 
 
@@ -103,22 +133,25 @@ def run_reference_arm(args):
         from pyoracle import Reference  # noqa: F401
     except Exception:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    cfg = CONFIGS[args.config]
+    L, k = cfg["L"], cfg["ref_step_mcs"]
     times, vals = [], []
     for i in range(args.warmup + args.steps):
-        v, el, w = reference_sample(mcs=10, mode=2, seed=1 + i)
+        v, el, w = reference_sample(cfg, mcs=k, mode=2, seed=1 + i)
         if i >= args.warmup:
             vals.append(v)
             times.append(el)
-    value = L * L * 10 * len(times) / sum(times)
+    value = L * L * k * len(times) / sum(times)
+    pub = published_rate(cfg)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "device": "host CPU (no GPU used)",
             "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": value / PUBLISHED_ATTEMPTS_PER_S, "dtype": "int32", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": value / pub if pub else None, "dtype": "int32", "data": "synthetic",
             "impl": "reference", "mcs_per_s": value / (L * L),
-            "config": workload_config({"step": "10 MCS of run_max_step (numRandoms = 5N: two double-buffered "
-                                               "batches) per step, window from the first density record"}),
+            "config": workload_config(cfg, {"step": "%d MCS of run_max_step (numRandoms = 5N: two double-buffered "
+                                                    "batches) per step, window from the first density record" % k}),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
-                             "sample": "10 MCS per step x %d steps, ThreadPool(%d)" % (args.steps, os.cpu_count())},
+                             "sample": "%d MCS per step x %d steps, ThreadPool(%d)" % (k, args.steps, os.cpu_count())},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -201,6 +234,45 @@ def ncu_traffic():
     return d.get("dram_bytes_per_launch"), d.get("mcs_per_launch")
 
 
+def band_measurement(e, cfg, model, rank, world, local, args):
+    """N > 1: the same lattice row-band sharded over the N ranks (bands.DistributedBand:
+    NCCL halo exchange of 12*kmcs rows per chunk, then the band kernel).  Device time, max over ranks,
+    of `steps` x 20 MCS; reported inside the replicas line (one JSON line per run)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_16639_b200 import bands
+
+    try:
+        L = cfg["L"]
+        p = e.SimParams(length=L, height=L, species=cfg["S"], mobility=cfg["M"], empty_prob=cfg["p0"], seed=20240601,
+                        mcs_limit=10 ** 12)
+        n = 20
+        with bands.DistributedBand(p, model, rank, world, device=local, kmcs=2) as b:
+            b.init_lattice()
+            for _ in range(max(1, args.warmup)):
+                b.advance(n)
+            torch.cuda.synchronize()
+            dist.barrier()
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(args.steps):
+                b.advance(n)
+            ev1.record()
+            torch.cuda.synchronize()
+            ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            ms = float(ms.item())
+            info = b.info
+        v = L * L * n * args.steps / (ms / 1e3)
+        return {"value": v, "unit": UNIT, "scaling": "strong", "ms_per_step": ms / args.steps, "mcs_per_step": n,
+                "mcs_per_s": v / (L * L), "kmcs": info["kmcs"], "halo_rows": info["halo"],
+                "workload": "one L=%d lattice row-band sharded over %d GPUs (bands.DistributedBand, NCCL halo "
+                            "exchange per %d-MCS chunk)" % (L, world, info["kmcs"])}
+    except Exception as ex:  # reported, never fatal to the replicas line
+        return {"value": None, "error": "%s: %s" % (type(ex).__name__, ex)}
+
+
 def run_ours(args):
     import torch
 
@@ -212,12 +284,14 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    cfg = CONFIGS[args.config]
+    L, S, MCS_PER_STEP = cfg["L"], cfg["S"], cfg["mcs_per_step"]
     seed = 20240601 + rank
-    model = e.make_circulant(3, [1])
-    params = e.SimParams(length=L, height=L, species=3, mobility=M, empty_prob=P0, num_randoms=NUM_RANDOMS,
-                         max_step=True, seed=seed, mcs_limit=10 ** 12)
+    model = e.make_circulant(3, [1]) if cfg["model"] == "rps" else e.make_rpsls()
+    params = e.SimParams(length=L, height=L, species=S, mobility=cfg["M"], empty_prob=cfg["p0"],
+                         num_randoms=cfg["num_randoms"], max_step=True, seed=seed, mcs_limit=10 ** 12)
     N = L * L
-    interval = e.align_num_randoms(NUM_RANDOMS, N) // N
+    interval = e.align_num_randoms(cfg["num_randoms"], N) // N
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
 
     eng = e.DeviceEngine(params, model, 1, device=local)
@@ -276,7 +350,7 @@ def run_ours(args):
     eng.close()
     cap = MCS_PER_STEP // interval + 2
     steps_buf = torch.empty(cap, dtype=torch.int64).pin_memory().numpy()
-    counts_buf = torch.empty(cap * 4, dtype=torch.int64).pin_memory().numpy().view(np.uint64)
+    counts_buf = torch.empty(cap * (S + 1), dtype=torch.int64).pin_memory().numpy().view(np.uint64)
     dom = np.ascontiguousarray(model.entries, np.float64)
     out_mcs, n_rec, status = C.c_int64(0), C.c_int64(0), C.c_int32(0)
     lib = _lib.lib()
@@ -286,7 +360,8 @@ def run_ours(args):
         p = e.SimParams(**{**params.__dict__, "mcs_limit": cur + MCS_PER_STEP}).to_c(seed)
         barrier()
         t0 = time.perf_counter()
-        _lib.check(lib.escg_simulate(C.byref(p), dom, 3, 0, int(e.EngineMode.MaxStep), local, _lib.ptr(lat_in), cur, 0, 0,
+        _lib.check(lib.escg_simulate(C.byref(p), dom, S, int(model.kind), int(e.EngineMode.MaxStep), local,
+                                     _lib.ptr(lat_in), cur, 0, 0,
                                      _lib.ptr(lat_out), C.byref(out_mcs), _lib.ptr(steps_buf), _lib.ptr(counts_buf), cap,
                                      C.byref(n_rec), C.byref(status)))
         t1 = time.perf_counter()
@@ -303,36 +378,44 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_value = N * MCS_PER_STEP * args.steps * world / e2e_s
     n_records = MCS_PER_STEP // interval + 1
+    band = band_measurement(e, cfg, model, rank, world, local, args) if world > 1 else None
 
     if rank == 0:
         peak, peak_src = peak_hbm()
         per_gpu = value / world
         traffic, tr_mcs = ncu_traffic()
+        kname = {"ring": "ring_kernel (persistent bit-sliced row bands, one launch per step)",
+                 "block": ("slice_kernel (bit-sliced overlapped-tile CRS, %d MCS/launch)" % desc.get("kmcs", 1)
+                           if desc.get("draw_format") == "sliced"
+                           else "block_kernel (overlapped-tile CRS, %d MCS/launch, %s draws)"
+                           % (desc.get("kmcs", 1), desc.get("draw_format"))),
+                 "tile": "tile_kernel (SMEM-resident lattice, persistent)"}[desc["kernel"]]
         roof = {"bound": "hbm", "achieved": per_gpu * 2 / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": per_gpu * 2 / 1e9 / peak, "peak_source": peak_src,
-                "traffic": traffic,
-                "kernel": ("slice_kernel (bit-sliced overlapped-tile CRS, %d MCS/launch)" if desc.get("draw_format") == "sliced"
-                           else "block_kernel (overlapped-tile CRS, %d MCS/launch)") % desc.get("kmcs", 1),
+                "traffic": traffic if args.config == "C3" else None,
+                "kernel": kname,
                 "algorithmic_bytes": "2 B per site-update attempt (1 B read + 1 B write of the uint8 lattice per "
                                      "site per MCS); achieved = attempts/s x 2 B over the device-timed region"
                                      + ("; during a run the lattice is held as 2-bit planes (0.5 B per attempt moved)"
                                         if desc.get("draw_format") == "sliced" else ""),
                 "avg_launch_us": total_ms / max(launches, 1) * 1e3,
-                "traffic_per_launch_mcs": tr_mcs}
+                "traffic_per_launch_mcs": tr_mcs if args.config == "C3" else None}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": value / PUBLISHED_ATTEMPTS_PER_S, "dtype": "u8",
-                "data": "synthetic (Philox-initialised random lattice, empty_prob 0.1)",
+                "scaling": "weak", "vs_baseline": value / published_rate(cfg) if published_rate(cfg) else None,
+                "dtype": "u8",
+                "data": "synthetic (Philox-initialised random lattice, empty_prob %g)" % cfg["p0"],
                 "mcs_per_s": value / N / world,
-                "config": workload_config({"parallelism": "replicas x%d (one lattice per GPU)" % world,
-                                           "kernel": desc}),
+                "config": workload_config(cfg, {"name": args.config,
+                                                "parallelism": "replicas x%d (one lattice per GPU)" % world,
+                                                "kernel": desc}),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * N,
-                        "d2h_bytes_per_step": 4 * N + n_records * (8 + 4 * 8) + 8,
+                        "d2h_bytes_per_step": 4 * N + n_records * (8 + (S + 1) * 8) + 8,
                         "path": "escg_simulate C ABI (simulate() mirror), pinned host int32 lattice in/out"},
                 "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
         # the binding limit: warp-instruction issue (148 SMs x 4 schedulers x 1 instr/clk); warp
         # instructions per attempt from the committed ncu capture of this kernel and launch shape
-        summ = ncu_summary()
+        summ = ncu_summary() if args.config == "C3" else {}
         clocks = line["clocks"]
         if summ.get("warp_inst_per_launch") and summ.get("mcs_per_launch") and clocks.get("sm_mhz"):
             wipa = summ["warp_inst_per_launch"] / (summ["mcs_per_launch"] * N)
@@ -342,9 +425,11 @@ def run_ours(args):
                              "frac": per_gpu * wipa / peak_issue,
                              "source": "ncu smsp__inst_executed.sum of one %d-MCS launch (profiles/ncu_summary.json)"
                                        % summ["mcs_per_launch"]}
+        if band is not None:
+            line["band"] = band
         if world == 1 and not args.no_cpu_baseline:
             try:
-                line["cpu_baseline"] = cpu_baseline()
+                line["cpu_baseline"] = cpu_baseline(cfg)
             except Exception as ex:  # reported, never fatal
                 line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                                         "sample": "unavailable: %s" % ex}
@@ -360,6 +445,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--config", default="C3", choices=sorted(CONFIGS),
+                    help="BASELINE.json configuration (default C3, the headline)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference_arm(args)

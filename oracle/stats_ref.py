@@ -14,7 +14,25 @@ from __future__ import annotations
 import math
 from typing import Sequence
 
-from paper_2508_16639_b200.experiments import MeanStd, mean_std  # noqa: F401  (stats.cpp:9-21 lives with the harness)
+from dataclasses import dataclass
+
+
+@dataclass
+class MeanStd:
+    mean: float = 0.0
+    std_dev: float = 0.0
+    n: int = 0
+
+
+def mean_std(xs: Sequence[float]) -> MeanStd:
+    """stats.cpp:9-21: sample mean and (n-1) standard deviation (0 when n < 2)."""
+    r = MeanStd(n=len(xs))
+    if not xs:
+        return r
+    r.mean = sum(xs) / len(xs)
+    if len(xs) >= 2:
+        r.std_dev = math.sqrt(sum((x - r.mean) ** 2 for x in xs) / (len(xs) - 1))
+    return r
 
 _EPS = 1e-15
 _TINY = 1e-300
@@ -108,3 +126,52 @@ def ks_two_sample_pvalue(a: Sequence[float], b: Sequence[float]) -> float:
         if term < 1e-12:
             break
     return min(1.0, max(0.0, p))
+
+
+def correlation_length(cells, length: int, height: int, rmax: int = 64) -> float:
+    """Spatial correlation length of one lattice (test-side observable, not a reference function):
+    C(r) = P(s(x) = s(x + r)) - sum_s rho_s^2 over horizontal and vertical periodic displacements r,
+    l = the first r with C(r) <= C(0)/e, linearly interpolated (rmax if never).  The same estimator
+    is applied to device and reference lattices, so only its distribution is compared."""
+    import numpy as np
+
+    a = np.asarray(cells).reshape(height, length)
+    rmax = min(rmax, min(length, height) // 4)
+    rho = np.bincount(a.ravel().astype(np.int64)) / a.size
+    base = float((rho ** 2).sum())
+    prev = None
+    c0 = None
+    for r in range(rmax + 1):
+        same = 0.5 * ((a == np.roll(a, r, axis=1)).mean() + (a == np.roll(a, r, axis=0)).mean())
+        c = same - base
+        if r == 0:
+            c0 = c
+            prev = c
+            continue
+        thr = c0 / math.e
+        if c <= thr:
+            return (r - 1) + (prev - thr) / (prev - c) if prev != c else float(r)
+        prev = c
+    return float(rmax)
+
+
+def bootstrap_threshold(grid, outcomes, n_boot: int = 2000, seed: int = 0):
+    """Mobility threshold = first M (ascending) with P(coexist) < 1/2, and its bootstrap distribution
+    (trials resampled with replacement per M).  outcomes[i] = 0/1 coexistence per trial at grid[i].
+    Returns (threshold or None, list of bootstrap thresholds, None where no M falls below 1/2)."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    grid = list(grid)
+
+    def thr(ps):
+        for m, p in zip(grid, ps):
+            if p < 0.5:
+                return m
+        return None
+
+    point = thr([float(np.mean(o)) for o in outcomes])
+    boots = []
+    for _ in range(n_boot):
+        boots.append(thr([float(np.mean(rng.choice(o, size=len(o), replace=True))) for o in outcomes]))
+    return point, boots

@@ -240,6 +240,50 @@ def gen_stats():
     return out
 
 
+# ---------------------------------------------------------------------------------------------
+# Round-2 ensembles: the regimes the fast kernels run in (bit-sliced: P(migration) >= 0.996; byte
+# block kernel below), with a spatial observable, and the C4 mobility sweep
+# ---------------------------------------------------------------------------------------------
+
+def _traj_corr(args):
+    L, M, p0, mcs, seed, every = args
+    import stats_ref
+
+    r = ref()
+    res = r.simulate(L, L, r.circulant(3, [1]), M, p0, mcs, seed, mode=0, want_cells=True)
+    idx = list(range(0, len(res["steps"]), every))
+    return ([res["counts"][i].tolist() for i in idx], res["steps"][idx].tolist(), res["status"],
+            stats_ref.correlation_length(res["cells"], L, L))
+
+
+C4_GRID = [1e-4, 2e-4, 3e-4, 4.5e-4, 6e-4, 8e-4, 1e-3, 1.5e-3, 3e-3]
+C4_SEEDS = {100: 64, 200: 64, 300: 32, 400: 32}
+
+
+def gen_stats2():
+    out = {}
+    with Pool(8) as pool:
+        for key, L, M, mcs, nseed, s0 in (("rps_L512_M1e-3", 512, 1e-3, 2000, 64, 5000),
+                                           ("rps_L1024_M3e-4", 1024, 3e-4, 1500, 48, 6000),
+                                           ("rps_L1024_M3e-5", 1024, 3e-5, 1500, 48, 7000)):
+            res = pool.map(_traj_corr, [(L, M, 0.1, mcs, s0 + s, 100) for s in range(nseed)])
+            out[key] = {"desc": "RPS L=%d M=%g p0=0.1, reference serial engine: counts every 100 MCS to %d, final "
+                                "status and correlation length (oracle/stats_ref.py)" % (L, M, mcs),
+                        "steps": res[0][1], "counts": [r_[0] for r_ in res], "status": [r_[2] for r_ in res],
+                        "corr_len": [r_[3] for r_ in res]}
+            print("done", key, flush=True)
+        c4 = {}
+        for L, nseed in C4_SEEDS.items():
+            by_m = {}
+            for i, M in enumerate(C4_GRID):
+                by_m[str(M)] = pool.map(_probe, [(M, L, 10000, 100000 + 1000 * i + L + s) for s in range(nseed)])
+            c4[str(L)] = by_m
+            print("done C4 L=%d" % L, flush=True)
+        out["c4_sweep_1e4mcs"] = {"desc": "C4: RPS L in 100..400, p0=0.1, 1e4 MCS, reference serial engine: "
+                                          "(alive species, status, last mcs) per seed", "grid": C4_GRID, "by_L": c4}
+    return out
+
+
 if __name__ == "__main__":
     def dump(name, obj):
         with open(os.path.join(HERE, name), "w") as f:
@@ -249,6 +293,9 @@ if __name__ == "__main__":
     dump("kat.json", gen_kat())
     dump("serial.json", gen_serial())
     dump("rule.json", gen_rule())
+    if "--stats2" in sys.argv:
+        dump("stats2.json", gen_stats2())
+        sys.exit(0)
     if "--stats" in sys.argv:
         dump("stats.json", gen_stats_seam(gen_stats()))
     elif "--stats-seam" in sys.argv:
