@@ -123,7 +123,7 @@ __device__ __forceinline__ void ring_publish(const RingCtx& C, int dir, int wrow
 // Import the neighbour's shared rows s_lo..s_hi of the previous phase (tag) into window rows
 // wrow0 + s; with nothing to import, wait for its header.  Polls until every word carries the tag.
 template <int NPL>
-__device__ __noinline__ void ring_import(const RingCtx& C, int src, int dir, int wrow0, int s_lo, int s_hi, int par,
+__device__ __forceinline__ void ring_import(const RingCtx& C, int src, int dir, int wrow0, int s_lo, int s_hi, int par,
                                          uint32_t tag, int diag_q) {
     const int lane = threadIdx.x & 31;
     const unsigned long long* mb = mailbox(C, src, dir, par);
@@ -333,16 +333,21 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
         __syncwarp();
         tbl = scratch;
     }
+    RDIAG(X.q, 1, clock64());
+    // the draws do not depend on the lattice: the neighbour's rows are awaited only now (before the
+    // draw words are loaded, so that few registers are live while polling)
+    if (X.imp) ring_import<NPL>(C, X.src, X.idir, X.iwrow0, X.is_lo, X.is_hi, X.ipar, X.itag,
+                                   static_cast<int>(X.q) - 800);
+    RDIAG(X.q, 2, clock64());
     uint32_t D[kDrawWords];
 #pragma unroll
     for (int i = 0; i < kDrawWords; ++i) D[i] = tbl[i * 32 + lane];
     const uint32_t Dm = valid ? (D[0] | D[1] | D[2] | D[3]) : 0u;
     const uint32_t act = ~Dm;
-    RDIAG(X.q, 1, clock64() + (Dm == 0x12345u));
-    // the draws do not depend on the lattice: the neighbour's rows are awaited only now
-    if (X.imp) ring_import<NPL>(C, X.src, X.idir, X.iwrow0, X.is_lo, X.is_hi, X.ipar, X.itag,
-                                   static_cast<int>(X.q) - 800);
-    RDIAG(X.q, 2, clock64());
+    // the exact low action bits of the lane's first undecided tile, drawn ahead of the footprint
+    // loads and the bit-parallel pass (its Philox latency would otherwise open the replay)
+    uint4 rf0 = make_uint4(0u, 0u, 0u, 0u);
+    if (Dm != 0u) rf0 = philox(item, c1, c2r | (static_cast<uint32_t>(__ffs(Dm) - 1) << 24), C.s32);
 
     uint32_t Q[4][NPL][4];
     uint32_t* rowp = C.sw + (wl - 1) * C.RP + lane * 4;
@@ -417,7 +422,7 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
                     << (4 * a);
             code |= ((D[a] >> l) & 1u) << (16 + a);
         }
-        const uint4 rf = philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), C.s32);
+        const uint4 rf = dm == Dm ? rf0 : philox(item, c1, c2r | (static_cast<uint32_t>(l) << 24), C.s32);
         tile_replay_regs<NPL>(F, l, code, rf, C);
     }
     RDIAG(X.q, 4, clock64() + (F[1][1][0] == 0x12345u));
