@@ -511,8 +511,48 @@ EXPORT void orc_crs_init(int length, int height, int species, double empty_prob,
  *         W[4a+1] (cell column), W[4a+2] | W[4a+3] << 1 (direction) and of W[16 + aK + i], i < K,
  *         as bit 31-i of the action word; its low 32-K bits are word a of SLICE_REF draw
  *         (c0 = item, attempt field l).
- * In every format the action word is a uniform 32-bit value assembled from disjoint Philox bits, so
- * the rule sees exactly the reference's action distribution. */
+ *  SLICED3 (fmt = 3 | K << 8; as SLICED): the undecided mask U_a of attempt a (bit l set:
+ *         tile l's action word has its top K bits all one) is drawn directly instead of as the AND
+ *         of K words: with T[0] = 2^32, T[g] = floor(T[g-1] (2^K - 1) / 2^K) (so T[g] / 2^32 =
+ *         (1 - 2^-K)^g within g 2^-32), a uniform word u gives the run of decided tiles from
+ *         position pos, G = #{g in [1, 32 - pos] : u < T[g]}; G = 32 - pos ends the mask, else bit
+ *         pos + G is set and the next run starts after it with the next word.  u_a = word a of
+ *         SLICE draw 4, the k-th next word of attempt a = word a of SLICE draw 5 + k.  Choice words
+ *         as SLICED (SLICE draws 0..3); an undecided attempt's action word is TK | (word a of the
+ *         SLICE_REF draw & ~TK), TK = the K leading ones; a decided attempt is a migration.
+ * In every format the action word is a uniform 32-bit value assembled from disjoint Philox bits (for
+ * SLICED3: the probability that an attempt is undecided is 2^-K within 2^-27, the reference's own
+ * float action quantisation being 2^-24), so the rule sees the reference's action distribution. */
+
+/* SLICED3 run thresholds T[1..32] for K action bits (T[0] = 2^32 implicit). */
+EXPORT void orc_slice3_table(int K, uint32_t* out32) {
+    uint64_t t = 1ull << 32;
+    for (int g = 1; g <= 32; ++g) {
+        t = (t * ((1ull << K) - 1ull)) >> K;
+        out32[g - 1] = (uint32_t)t;
+    }
+}
+
+/* SLICED3 undecided mask of attempt a of an item (see above). */
+static uint32_t slice3_mask(uint64_t seed, uint32_t item, uint64_t mcs, uint32_t p, int a, uint32_t u,
+                            const uint32_t* T) {
+    uint32_t U = 0;
+    int pos = 0, k = 0;
+    for (;;) {
+        const int rem = 32 - pos;
+        int G = 0;
+        while (G < rem && u < T[G]) ++G; /* T[G] = threshold of run length G + 1 */
+        if (G == rem) break;
+        pos += G;
+        U |= 1u << pos;
+        if (++pos == 32) break;
+        uint32_t w4[4];
+        crs_draw(seed, item, mcs, DOM_SLICE, p, (uint32_t)(5 + k), w4);
+        u = w4[a];
+        ++k;
+    }
+    return U;
+}
 static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a, uint32_t* low, uint32_t* hi_part,
                              int* hi_shift) {
     if (!narrow) {
@@ -525,6 +565,14 @@ static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a
         *hi_part = half >> lb;
         *hi_shift = 32 - (16 - lb);
     }
+}
+
+/* Test hook: the SLICED3 undecided mask of attempt a of item `item` in phase p of MCS mcs. */
+EXPORT uint32_t orc_slice3_mask(uint64_t seed, uint32_t item, uint64_t mcs, uint32_t p, int a, int K) {
+    uint32_t T3[32], w4[4];
+    orc_slice3_table(K, T3);
+    crs_draw(seed, item, mcs, DOM_SLICE, p, 4u, w4);
+    return slice3_mask(seed, item, mcs, p, a, w4[a], T3);
 }
 
 /* n_mcs rounds of the coloured random-sequential schedule starting at MCS mcs0, applying the
@@ -540,9 +588,13 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
     if (periodic && (length < 4 || height < 4)) return 2;
     int seam_y = -1, seam_x = -1;
     const int ncy = periodic ? crs_axis(height, &seam_y) : 2, ncx = periodic ? crs_axis(length, &seam_x) : 2;
-    const int narrow = (fmt & 0xFF) == 1, sliced = (fmt & 0xFF) == 2, K = fmt >> 8;
+    const int narrow = (fmt & 0xFF) == 1, sliced = (fmt & 0xFF) == 2 || (fmt & 0xFF) == 3, K = fmt >> 8;
+    const int sliced3 = (fmt & 0xFF) == 3;
     if (narrow && (ncy != 2 || ncx != 2 || length % 8 != 0)) return 2;
     if (sliced && (ncy != 2 || ncx != 2 || length % 128 != 0 || arity != 4 || K < 1 || K > 24)) return 2;
+    uint32_t T3[32];
+    if (sliced3) orc_slice3_table(K, T3);
+    const uint32_t TK = K >= 32 ? ~0u : ~((1u << (32 - K)) - 1u);
     orc_ctx_make(&c, length, height, species, arity, flux, dom, mobility);
     for (int64_t mcs = mcs0; mcs < mcs0 + n_mcs; ++mcs) {
         int oy, ox, perm[9];
@@ -558,14 +610,17 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
                     const uint32_t tile = (uint32_t)ty * (uint32_t)tx_n + (uint32_t)tx;
                     const uint32_t sid = narrow ? (uint32_t)ty * (uint32_t)tq + (uint32_t)(tx >> 2) : tile;
                     const int h = (tx >> 1) & 1;
-                    uint32_t w[4], sw[4 * (4 + 24)], srf[4];
+                    uint32_t w[4], sw[4 * (4 + 24)], srf[4], U3[4] = {0, 0, 0, 0};
                     int lane = 0;
                     if (sliced) {
                         const int ax = ((2 * tx - ox) % length + length) % length;
                         const uint32_t item = (uint32_t)ty * (uint32_t)(length / 128) + (uint32_t)(ax >> 7);
                         lane = (ax & 127) >> 2;
-                        for (int j = 0; j < 4 + K; ++j)
+                        for (int j = 0; j < (sliced3 ? 5 : 4 + K); ++j)
                             crs_draw(seed, item, (uint64_t)mcs, DOM_SLICE, (uint32_t)p, (uint32_t)j, sw + 4 * j);
+                        if (sliced3)
+                            for (int a = 0; a < 4; ++a)
+                                U3[a] = slice3_mask(seed, item, (uint64_t)mcs, (uint32_t)p, a, sw[16 + a], T3);
                         crs_draw(seed, item, (uint64_t)mcs, DOM_SLICE_REF, (uint32_t)p, (uint32_t)lane, srf);
                     } else {
                         crs_draw(seed, sid, (uint64_t)mcs, DOM_STEP, (uint32_t)p, 0, w);
@@ -579,9 +634,14 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
                             dy = (int)((sw[4 * a] >> lane) & 1u);
                             dx = (int)((sw[4 * a + 1] >> lane) & 1u);
                             dir = (int)(((sw[4 * a + 2] >> lane) & 1u) | (((sw[4 * a + 3] >> lane) & 1u) << 1));
-                            uint32_t hi = 0;
-                            for (int i = 0; i < K; ++i) hi = (hi << 1) | ((sw[16 + a * K + i] >> lane) & 1u);
-                            x = (hi << (32 - K)) | (srf[a] & ((1u << (32 - K)) - 1u));
+                            if (sliced3) {
+                                /* decided: a certain migration (action word 0); undecided: the exact word */
+                                x = ((U3[a] >> lane) & 1u) ? (TK | (srf[a] & ~TK)) : 0u;
+                            } else {
+                                uint32_t hi = 0;
+                                for (int i = 0; i < K; ++i) hi = (hi << 1) | ((sw[16 + a * K + i] >> lane) & 1u);
+                                x = (hi << (32 - K)) | (srf[a] & ((1u << (32 - K)) - 1u));
+                            }
                         } else {
                             crs_attempt_bits(narrow, lb, w, h, a, &low, &hi_part, &hi_shift);
                             dir = (int)(low & (uint32_t)(arity - 1));

@@ -93,6 +93,9 @@ class Oracle:
                                   C.c_int64, C.c_int64, C.c_int]
         L.orc_seed32.restype = C.c_uint32
         L.orc_seed32.argtypes = [C.c_uint64]
+        L.orc_slice3_table.argtypes = [C.c_int, _u32]
+        L.orc_slice3_mask.restype = C.c_uint32
+        L.orc_slice3_mask.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_int, C.c_int]
 
     # --- RNG -----------------------------------------------------------------------------
     def mt_words(self, seed32, n):
@@ -174,6 +177,15 @@ class Oracle:
         self.lib.orc_crs_round_g(seed, mcs, ncy, ncx, C.byref(oy), C.byref(ox), perm)
         return oy.value, ox.value, perm[:ncy * ncx].tolist()
 
+    def slice3_table(self, K):
+        """SLICED3 run thresholds T[1..32] (escg_oracle.c orc_slice3_table)."""
+        out = np.zeros(32, np.uint32)
+        self.lib.orc_slice3_table(K, out)
+        return out
+
+    def slice3_mask(self, seed, item, mcs, phase, attempt, K):
+        return int(self.lib.orc_slice3_mask(seed, item, mcs, phase, attempt, K))
+
     def crs_init(self, length, height, species, empty_prob, seed):
         cells = np.zeros(length * height, np.int32)
         self.lib.orc_crs_init(length, height, species, empty_prob, seed, cells)
@@ -181,7 +193,7 @@ class Oracle:
 
     def crs_run(self, cells, length, height, dom, mobility, seed, mcs0, n_mcs, arity=4, flux=True, narrow=False):
         """`narrow`: draw format — False/True (WIDE/NARROW) or the engine's draw code
-        (DeviceEngine.draw_code(): 0 WIDE, 1 NARROW, 2 | K << 8 SLICED)."""
+        (DeviceEngine.draw_code(): 0 WIDE, 1 NARROW, 2 | K << 8 SLICED, 3 | K << 8 SLICED3)."""
         species = int(round(np.sqrt(np.asarray(dom).size)))
         cells = np.ascontiguousarray(cells, np.int32).copy()
         rc = self.lib.orc_crs_run(cells, length, height, species, arity, int(flux),

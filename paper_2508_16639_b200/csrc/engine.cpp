@@ -137,6 +137,16 @@ Thresholds compute_thresholds(double mobility, int64_t cells, const double* dom,
 }
 
 // min{x : double(float(x)/4294967295.0f) >= p0} — the empty test of init_lattice (lattice.hpp:59).
+// SLICED3 run thresholds T[g-1] = floor((1 - 2^-K)^g 2^32) by the recurrence t_g = floor(t_{g-1}
+// (2^K - 1) / 2^K), t_0 = 2^32 (oracle/escg_oracle.c orc_slice3_table; within g 2^-32 of the exact power).
+void slice3_table(int K, uint32_t* out32) {
+    uint64_t t = 1ull << 32;
+    for (int g = 1; g <= 32; ++g) {
+        t = (t * ((1ull << K) - 1ull)) >> K;
+        out32[g - 1] = static_cast<uint32_t>(t);
+    }
+}
+
 uint32_t empty_threshold(double p0) {
     if (!(p0 > 0.0)) return 0u;
     const uint64_t v = lower_bound_u32(0, uint64_t{1} << 32, [&](uint32_t x) {
@@ -189,6 +199,7 @@ struct escg_dev {
     int npl = 2;     // SLICED: species-code bit planes
     int lpi = 1;     // SLICED: lanes per item (slice.cu)
     int qcap = 0;    // SLICED: deferred-tile queue capacity override (tests)
+    bool sliced3 = false;  // SLICED3 draws (undecided masks drawn directly)
     int kmcs = 1;    // block kernel: MCS per launch (temporal blocking)
     bool persist = false;  // block kernel runs as one persistent cooperative launch per run/advance
     // SLICED single lattices on the persistent ring kernel (ring.cu): bands, shared memory, mailboxes
@@ -226,6 +237,7 @@ struct escg_dev {
     DevBuf<int32_t> d_i32;
     DevBuf<unsigned long long> d_mbox;
     DevBuf<unsigned int> d_decided;
+    DevBuf<uint32_t> d_T3;
     int64_t trace_cap = 0;
     bool traced = false;
     double last_ms = 0.0;
@@ -521,6 +533,7 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
     a.npl = h->npl;
     a.lpi = h->lpi;
     a.qcap = h->qcap;
+    a.T3 = h->sliced3 ? h->d_T3.p : nullptr;
     a.step = 1;
     int64_t launches = 0;
     for (int64_t done = 0; done < n;) {
@@ -570,6 +583,7 @@ void enqueue_ring(escg_dev* h, int64_t t0, int64_t t1, int record, const escgd::
     a.ticket = h->d_ticket.p;
     a.smem_bytes = h->ring_smem;
     a.qcap = h->qcap;
+    a.T3 = h->sliced3 ? h->d_T3.p : nullptr;
     CK(cudaMemsetAsync(h->d_mbox.p, 0, sizeof(unsigned long long) * h->d_mbox.n, h->stream));
     CK(cudaMemsetAsync(h->d_decided.p, 0, sizeof(unsigned int), h->stream));
     CK(escgd::launch_ring(a, h->ring_nb, h->stream));
@@ -1014,6 +1028,9 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 h->lpi = 1;
                 if (const char* lv = std::getenv("ESCG_SLICE_LPI")) h->lpi = (h->npl == 2 && std::atoi(lv) == 2) ? 2 : 1;
                 if (const char* qv = std::getenv("ESCG_SLICE_QCAP")) h->qcap = std::atoi(qv);
+                // SLICED3 by default: one draw word per attempt for the undecided masks instead of K
+                // (ESCG_SLICE_DRAWS=2 keeps the K action words of SLICED)
+                h->sliced3 = !(std::getenv("ESCG_SLICE_DRAWS") && std::atoi(std::getenv("ESCG_SLICE_DRAWS")) == 2);
             }
         }
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -1088,6 +1105,12 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             }
             h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
             h->d_ticket.alloc(n_replicas);
+        }
+        if (h->sliced3) {
+            uint32_t t3[32];
+            slice3_table(h->K, t3);
+            h->d_T3.alloc(32);
+            CK(cudaMemcpy(h->d_T3.p, t3, sizeof(t3), cudaMemcpyHostToDevice));
         }
         h->d_seeds.alloc(n_replicas);
         h->d_last.alloc(static_cast<size_t>(h->S1) * n_replicas);
@@ -1524,6 +1547,7 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
                 a.npl = h->npl;
                 a.lpi = h->lpi;
                 a.qcap = h->qcap;
+                a.T3 = h->sliced3 ? h->d_T3.p : nullptr;
                 a.dst_index = 1 - par;
                 a.mcs = t0 + done;
                 a.nmcs = chunk;
@@ -1614,6 +1638,7 @@ int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
         a.npl = h->npl;
         a.lpi = h->lpi;
         a.qcap = h->qcap;
+        a.T3 = h->sliced3 ? h->d_T3.p : nullptr;
         a.dst_index = 1 - par;
         a.mcs = h->mcs[0];
         a.nmcs = n_mcs;
@@ -1634,7 +1659,7 @@ int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
 int escg_dev_draw_format(escg_dev* h, int32_t* narrow) {
     return guarded([&] {
         if (!h || !narrow) config_error("null argument");
-        *narrow = h->narrow == 2 ? (2 | (h->K << 8)) : h->narrow;
+        *narrow = h->narrow == 2 ? ((h->sliced3 ? 3 : 2) | (h->K << 8)) : h->narrow;
     });
 }
 

@@ -88,6 +88,7 @@ struct RingCtx {
     int S1;
     unsigned long long* mbox;
     int mbs;
+    const uint32_t* T3;  // SLICED3 run thresholds in shared memory, null: SLICED
 };
 
 // Mailbox of band `cta`, direction dir (0: rows shared with the band above, 1: below), parity par.
@@ -228,16 +229,23 @@ __device__ __forceinline__ void put_all(uint32_t (&Q)[4][NPL][4], const uint32_t
 // The SLICED draws of one item (slice.cu slice_phase, LPI = 1): K action words AND-ed into the
 // undecided masks U, then the choice planes (cell row, cell column, direction bits) per attempt.
 template <int K>
-__device__ __forceinline__ void slab_draws(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32,
+__device__ __forceinline__ void slab_draws(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* T3,
                                            uint32_t (&D)[kDrawWords]) {
+    if (T3 != nullptr) {  // SLICED3: the undecided masks drawn directly (slice_common.cuh)
+        uint32_t U[4];
+        slice3_masks(item, c1, c2s, s32, T3, U);
 #pragma unroll
-    for (int a = 0; a < 4; ++a) D[a] = ~0u;
+        for (int a = 0; a < 4; ++a) D[a] = U[a];
+    } else {
 #pragma unroll
-    for (int jj = 0; jj < K; ++jj) {
-        const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(4 + jj) << 24), s32);
-        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+        for (int a = 0; a < 4; ++a) D[a] = ~0u;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) D[(4 * jj + c) / K] &= vw[c];
+        for (int jj = 0; jj < K; ++jj) {
+            const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(4 + jj) << 24), s32);
+            const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) D[(4 * jj + c) / K] &= vw[c];
+        }
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -252,9 +260,10 @@ __device__ __forceinline__ void slab_draws(uint32_t item, uint32_t c1, uint32_t 
 // The draws of one slab item into shared memory ([word][lane]); out of line so the kernel holds a
 // single copy of the Philox code.
 template <int K>
-__device__ __noinline__ void draws_to_smem(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, uint32_t* t) {
+__device__ __noinline__ void draws_to_smem(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* T3,
+                                           uint32_t* t) {
     uint32_t D[kDrawWords];
-    slab_draws<K>(item, c1, c2s, s32, D);
+    slab_draws<K>(item, c1, c2s, s32, T3, D);
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < kDrawWords; ++i) t[i * 32 + lane] = D[i];
@@ -329,7 +338,7 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
     RDIAG(X.q, 0, clock64());
 
     if (tbl == nullptr) {  // not drawn ahead by a producer warp: draw now (this warp's scratch)
-        draws_to_smem<K>(item, c1, c2s, C.s32, scratch);
+        draws_to_smem<K>(item, c1, c2s, C.s32, C.T3, scratch);
         __syncwarp();
         tbl = scratch;
     }
@@ -495,6 +504,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     __shared__ uint32_t sScr[kRingWarps][kDrawWords * 32];  // slab warps' own draws
     __shared__ uint32_t sCnt[1 << NPL];
     __shared__ int sStop;
+    __shared__ uint32_t sT3[32];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x, nb = gridDim.x;
     const int H = a.H, GL = a.L >> 7, S1 = a.S + 1;
@@ -503,6 +513,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     const int band = R1 - R0, RP = NPL * GL * 4, per_row = NPL * GL;
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
     for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
+    if (a.T3 != nullptr && tid < 32) sT3[tid] = a.T3[tid];
     if (*reinterpret_cast<volatile const int32_t*>(a.run.status) != kStatusRunning) return;  // uniform
 
     for (int idx = tid; idx < (band + 3) * per_row; idx += nt) {  // rows R0-1 .. R1+1 (mod H)
@@ -534,6 +545,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     C.S1 = S1;
     C.mbox = a.mbox;
     C.mbs = a.mbs;
+    C.T3 = a.T3 != nullptr ? sT3 : nullptr;
     const int up = c == 0 ? nb - 1 : c - 1, down = c == nb - 1 ? 0 : c + 1;
     const int64_t interval = a.run.interval > 0 ? a.run.interval : 1;
     // two warps beyond the most slabs a phase can have draw the next phase's boundary slabs
@@ -634,7 +646,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
                 j = j >= C.Hh ? j - C.Hh : j;
                 const uint32_t item = static_cast<uint32_t>(j) * static_cast<uint32_t>(GL) + static_cast<uint32_t>(lane);
                 draws_to_smem<K>(item, static_cast<uint32_t>(mn),
-                                 ctr2(static_cast<uint64_t>(mn), kDomSlice, static_cast<uint32_t>(pn), 0u), C.s32,
+                                 ctr2(static_cast<uint64_t>(mn), kDomSlice, static_cast<uint32_t>(pn), 0u), C.s32, C.T3,
                                  sDraw[par ^ 1][warp == wtop ? 0 : 1]);
             }
             if (snap && a.record) {

@@ -86,6 +86,7 @@ struct SliceCtx {
     uint4* q;             // deferred-tile queue of the phase: (w | acol << 16, code, item)
     unsigned* qn;         // its fill count
     unsigned qcap;        // its capacity (<= kSliceQueue; smaller in tests of the overflow path)
+    const uint32_t* T3;   // SLICED3 run thresholds in shared memory, null: SLICED (K action words)
 };
 
 // Out-of-line copy for the in-place overflow path inside the (per-residue) phase bodies.
@@ -125,14 +126,18 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         // choice planes (draws 0..3): cell row, cell column, direction bits
         uint32_t U[4], Y[4], X[4], D0[4], D1[4];
         if constexpr (LPI == 1) {
+            if (C.T3 != nullptr) {
+                slice3_masks(item, c1, c2s, C.s32, C.T3, U);
+            } else {
 #pragma unroll
-            for (int a = 0; a < 4; ++a) U[a] = ~0u;
+                for (int a = 0; a < 4; ++a) U[a] = ~0u;
 #pragma unroll
-            for (int jj = 0; jj < K; ++jj) {
-                const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(4 + jj) << 24), C.s32);
-                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+                for (int jj = 0; jj < K; ++jj) {
+                    const uint4 v = philox(item, c1, c2s | (static_cast<uint32_t>(4 + jj) << 24), C.s32);
+                    const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) U[(4 * jj + c) / K] &= vw[c];
+                    for (int c = 0; c < 4; ++c) U[(4 * jj + c) / K] &= vw[c];
+                }
             }
 #pragma unroll
             for (int a = 0; a < 4; ++a) {
@@ -145,13 +150,18 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         } else {
             // lane h: attempts 2h, 2h+1 (action words [2hK, 2hK + 2K) = draws 4 + hK/2 .. 4 + hK/2 + K/2 - 1)
             uint32_t Ul[2] = {~0u, ~0u};
+            uint32_t U3[4];
+            if (C.T3 != nullptr) {
+                slice3_masks(item, c1, c2s, C.s32, C.T3, U3);  // both lanes of the pair (same masks)
+            } else {
 #pragma unroll
-            for (int t = 0; t < K / 2; ++t) {
-                const uint32_t jj = 4u + static_cast<uint32_t>(h * (K / 2) + t);
-                const uint4 v = philox(item, c1, c2s | (jj << 24), C.s32);
-                const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+                for (int t = 0; t < K / 2; ++t) {
+                    const uint32_t jj = 4u + static_cast<uint32_t>(h * (K / 2) + t);
+                    const uint4 v = philox(item, c1, c2s | (jj << 24), C.s32);
+                    const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-                for (int c = 0; c < 4; ++c) Ul[(4 * t + c) / K] &= vw[c];
+                    for (int c = 0; c < 4; ++c) Ul[(4 * t + c) / K] &= vw[c];
+                }
             }
             const uint4 v0 = philox(item, c1, c2s | (static_cast<uint32_t>(2 * h) << 24), C.s32);
             const uint4 v1 = philox(item, c1, c2s | (static_cast<uint32_t>(2 * h + 1) << 24), C.s32);
@@ -159,7 +169,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
             for (int a = 0; a < 4; ++a) {
                 const int src = pbase + (a >> 1);
                 const uint4 v = (a & 1) ? v1 : v0;
-                U[a] = __shfl_sync(kFull, Ul[a & 1], src);
+                U[a] = C.T3 != nullptr ? U3[a] : __shfl_sync(kFull, Ul[a & 1], src);
                 Y[a] = __shfl_sync(kFull, v.x, src);
                 X[a] = __shfl_sync(kFull, v.y, src);
                 D0[a] = __shfl_sync(kFull, v.z, src);
@@ -299,6 +309,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     __shared__ uint32_t sTh[(kMaxSliceSpecies + 1) * (kMaxSliceSpecies + 1)];
     __shared__ uint4 sQ[kSliceQueue];
     __shared__ unsigned sQn[3];
+    __shared__ uint32_t sT3[32];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int r = blockIdx.z, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     // local rows (the buffer; band engines: halo + band + halo, never wrapped) vs global rows (draws)
@@ -318,6 +329,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
     if (tid < 3) sQn[tid] = 0u;
     for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
+    if (a.T3 != nullptr && tid < 32) sT3[tid] = a.T3[tid];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
 
@@ -354,6 +366,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
         C.sT = smem_addr(sTh);
         C.q = sQ;
         C.qcap = a.qcap > 0 && a.qcap < static_cast<int>(kSliceQueue) ? static_cast<unsigned>(a.qcap) : kSliceQueue;
+        C.T3 = a.T3 != nullptr ? sT3 : nullptr;
         C.S1 = S1;
 #pragma unroll 1
         for (int t = 0; t < a.nmcs; ++t) {

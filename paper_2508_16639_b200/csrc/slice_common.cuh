@@ -207,3 +207,50 @@ __device__ __forceinline__ void slice_replay_group(uint32_t sw0, int RP, int Gw,
 
 }  // namespace
 }  // namespace escgd
+
+namespace escgd {
+namespace {
+
+// SLICED3 draws (oracle/escg_oracle.c slice3_mask is the definition): the undecided
+// mask U_a of an item's attempt a — bit l set iff tile l's action word has its K top bits all one,
+// i.i.d. with probability 2^-K — drawn directly from one word instead of as the AND of K words.
+// T (shared memory, 32 words): T[g-1] = floor((1 - 2^-K)^g 2^32) by the recurrence of
+// orc_slice3_table; u < T[g-1] means "the next g tiles are decided".
+__device__ __noinline__ uint32_t slice3_rare(uint32_t u, int a, uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32,
+                                             const uint32_t* T) {
+    uint32_t U = 0;
+    int pos = 0, k = 0;
+    for (;;) {
+        const int rem = 32 - pos;
+        int lo = 0, hi = rem;  // G = the longest run g <= rem with u < T[g-1] (T decreasing)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (u < T[mid - 1])
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        if (lo == rem) break;
+        pos += lo;
+        U |= 1u << pos;
+        if (++pos == 32) break;
+        const uint4 w = philox(item, c1, c2s | ((5u + static_cast<uint32_t>(k)) << 24), s32);
+        u = a == 0 ? w.x : (a == 1 ? w.y : (a == 2 ? w.z : w.w));
+        ++k;
+    }
+    return U;
+}
+
+// The four attempts' undecided masks of an item: SLICE draw 4 gives u_0..u_3; a word below T[31]
+// (32 decided tiles, P = (1 - 2^-K)^32) is the common case and costs one comparison.
+__device__ __forceinline__ void slice3_masks(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* T,
+                                             uint32_t (&U)[4]) {
+    const uint4 v = philox(item, c1, c2s | (4u << 24), s32);
+    const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+    const uint32_t t32 = T[31];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) U[a] = u[a] < t32 ? 0u : slice3_rare(u[a], a, item, c1, c2s, s32, T);
+}
+
+}  // namespace
+}  // namespace escgd

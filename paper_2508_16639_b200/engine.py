@@ -421,7 +421,8 @@ class DeviceEngine:
 
     def draw_code(self) -> int:
         """The draw format as the oracle names it (oracle/escg_oracle.c orc_crs_run `fmt`):
-        0 WIDE, 1 NARROW, 2 | K << 8 SLICED with K action bit planes."""
+        0 WIDE, 1 NARROW, 2 | K << 8 SLICED with K action bit planes, 3 | K << 8 SLICED3 (undecided masks
+        drawn directly)."""
         v = C.c_int32(0)
         check(lib().escg_dev_draw_format(self._h, C.byref(v)))
         return int(v.value)
@@ -429,7 +430,7 @@ class DeviceEngine:
     def draw_format(self) -> str:
         """'wide', 'narrow' or 'sliced' — which attempt-word layout this engine's
         draws use."""
-        return {0: "wide", 1: "narrow", 2: "sliced"}[self.draw_code() & 0xFF]
+        return {0: "wide", 1: "narrow", 2: "sliced", 3: "sliced"}[self.draw_code() & 0xFF]
 
     def describe(self):
         vals = [C.c_int32(0) for _ in range(4)]

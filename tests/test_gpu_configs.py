@@ -31,8 +31,8 @@ def _run_records(oracle, init, L, H, dom, M, seed, code, S, mcs0, bounds):
 
 def test_c3_bench_configuration_matches_oracle(escg, oracle):
     """The bench kernel as planned (bit-sliced, K=10, 2 MCS per launch) with the bench's own record
-    cadence: advance(4), then run to MCS 22 with interval 9 (records at 4, 13, 22; each 9-MCS
-    interval runs as launches of 2+2+2+2+1 MCS), every record and both lattices against the oracle."""
+    cadence: advance(4), then run to MCS 22 with interval 9 (records at 4, 13, 22), every record and
+    both lattices against the oracle."""
     L, M, p0, seed = 3200, 1e-4, 0.1, 20240601
     model = escg.make_circulant(3, [1])
     p = escg.SimParams(length=L, height=L, species=3, mobility=M, empty_prob=p0, num_randoms=100000000,
@@ -42,7 +42,7 @@ def test_c3_bench_configuration_matches_oracle(escg, oracle):
     with escg.DeviceEngine(p, model) as eng:
         d = eng.describe()
         code = eng.draw_code()
-        assert code == 2 | (10 << 8), hex(code)
+        assert code == 3 | (10 << 8), hex(code)  # SLICED3, K = 10 action bits
         assert d["kernel"] in ("block", "ring") and d["draw_format"] == "sliced", d
         eng.init_lattice()
         init = eng.get_lattice()

@@ -662,14 +662,17 @@ SLICED_CASES = [
 ]
 
 
-@pytest.mark.parametrize("lpi,qcap", [("1", None), ("1", "1"), ("2", None), ("2", "3")])
+@pytest.mark.parametrize("lpi,qcap,draws", [("1", None, "3"), ("1", "1", "3"), ("2", None, "3"), ("2", "3", "3"),
+                                             ("1", None, "2"), ("2", None, "2")])
 @pytest.mark.parametrize("case", SLICED_CASES, ids=[f"{c[0]}x{c[1]}_{c[5]}_K{c[8]}" for c in SLICED_CASES])
-def test_slice_kernel_matches_crs_oracle(escg, oracle, case, lpi, qcap, monkeypatch):
-    """The bit-sliced block kernel == oracle orc_crs_run with the SLICED draw spec, bit for bit:
-    advance in two calls (bytes -> planes -> bytes between them), then run() with records.  One
-    and two lanes per item; a 3-entry deferred-tile queue forces the in-place overflow path."""
+def test_slice_kernel_matches_crs_oracle(escg, oracle, case, lpi, qcap, draws, monkeypatch):
+    """The bit-sliced block kernel == oracle orc_crs_run with the SLICED3 (default) or SLICED draw
+    spec, bit for bit: advance in two calls (bytes -> planes -> bytes between them), then run() with
+    records.  One and two lanes per item; a 3-entry deferred-tile queue forces the in-place overflow
+    path."""
     L, H, S, M, p0, name, split, kmax, K = case
     monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    monkeypatch.setenv("ESCG_SLICE_DRAWS", draws)
     monkeypatch.setenv("ESCG_SLICE_LPI", lpi)
     if qcap:
         monkeypatch.setenv("ESCG_SLICE_QCAP", qcap)
@@ -682,7 +685,7 @@ def test_slice_kernel_matches_crs_oracle(escg, oracle, case, lpi, qcap, monkeypa
     p = params(escg, L, H, S, M, p0, 4, True, seed=seed, mcs=12)
     with escg.DeviceEngine(p, model, kernel="block") as eng:
         code = eng.draw_code()
-        assert code == 2 | (K << 8), hex(code)
+        assert code == int(draws) | (K << 8), hex(code)
         if split:
             assert eng.describe()["ctas"] == int(split.split(",")[0]) * int(split.split(",")[1])
         eng.init_lattice()
@@ -717,7 +720,7 @@ def test_slice_kernel_forced_action_planes(escg, oracle, kforce, kwant, monkeypa
     p = params(escg, L, H, 3, M, 0.1, 4, True, seed=29, mcs=4)
     with escg.DeviceEngine(p, model, kernel="block") as eng:
         code = eng.draw_code()
-        assert code == 2 | (kwant << 8), hex(code)
+        assert code == 3 | (kwant << 8), hex(code)
         eng.init_lattice()
         init = eng.get_lattice()
         eng.advance(3)

@@ -31,13 +31,14 @@ def _params(escg, L, H, S, M, p0, seed, mcs):
     return escg.SimParams(length=L, height=H, species=S, mobility=M, empty_prob=p0, seed=seed, mcs_limit=mcs)
 
 
-@pytest.mark.parametrize("qcap", [None, "1"])
+@pytest.mark.parametrize("qcap,draws", [(None, "3"), ("1", "3"), (None, "2")])
 @pytest.mark.parametrize("case", RING_CASES, ids=[f"{c[0]}x{c[1]}_{c[5]}_nb{c[6]}" for c in RING_CASES])
-def test_ring_matches_crs_oracle(escg, oracle, case, qcap, monkeypatch):
+def test_ring_matches_crs_oracle(escg, oracle, case, qcap, draws, monkeypatch):
     """advance(3), advance(4), then run(12, interval=2): lattices and every record against the
     oracle.  qcap=1 shrinks the per-warp deferred-tile queue so the in-place replay runs."""
     L, H, S, M, p0, name, nb, K = case
     monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    monkeypatch.setenv("ESCG_SLICE_DRAWS", draws)  # SLICED3 (default) and SLICED
     if nb:
         monkeypatch.setenv("ESCG_RING_NB", nb)
     if qcap:
@@ -47,7 +48,7 @@ def test_ring_matches_crs_oracle(escg, oracle, case, qcap, monkeypatch):
     with escg.DeviceEngine(_params(escg, L, H, S, M, p0, seed, 12), model, kernel="ring") as eng:
         d = eng.describe()
         code = eng.draw_code()
-        assert d["kernel"] == "ring" and code & 0xFF == 2 and (K is None or code >> 8 == K), (d, hex(code))
+        assert d["kernel"] == "ring" and code & 0xFF == int(draws) and (K is None or code >> 8 == K), (d, hex(code))
         if nb:
             assert d["ctas"] == int(nb)
         eng.init_lattice()

@@ -255,3 +255,41 @@ def test_oracle_matches_compiled_reference(oracle, ref):
     b = ref.simulate(32, 24, D, 1e-3, 0.1, 30, 77)
     assert np.array_equal(a["cells"], b["cells"]) and np.array_equal(a["counts"], b["counts"])
     assert np.array_equal(ref.init_lattice(20, 20, 5, 0.2, 3), oracle.serial_draws(20, 20, 5, 0.2, 3, 0)[0])
+
+
+def test_slice3_thresholds_track_the_exact_powers(oracle):
+    """SLICED3 run thresholds (escg_oracle.c orc_slice3_table): T[g-1] within g of floor((1-2^-K)^g 2^32)."""
+    from fractions import Fraction
+
+    for K in (6, 8, 10, 12, 14, 16):
+        t = oracle.slice3_table(K)
+        for g in range(1, 33):
+            exact = int(Fraction(2 ** K - 1, 2 ** K) ** g * 2 ** 32)
+            assert exact - g <= int(t[g - 1]) <= exact, (K, g)
+
+
+@pytest.mark.parametrize("K", [6, 8])
+def test_slice3_masks_are_iid_bernoulli(oracle, K):
+    """The SLICED3 undecided mask of an attempt has i.i.d. Bernoulli(2^-K) bits: the count of set bits
+    per mask is Binomial(32, 2^-K) and every bit position is equally likely (chi-square)."""
+    import math
+
+    q = 2.0 ** -K
+    n = 40000
+    pos = np.zeros(32)
+    zeros = ones = multi = 0
+    for i in range(n):
+        u = oracle.slice3_mask(77, i, 5, i % 4, i % 4, K)
+        c = bin(u).count("1")
+        zeros += c == 0
+        ones += c == 1
+        multi += c >= 2
+        for b in range(32):
+            pos[b] += (u >> b) & 1
+    p0 = (1 - q) ** 32
+    p1 = 32 * q * (1 - q) ** 31
+    for k, p in ((zeros, p0), (ones, p1), (multi, 1 - p0 - p1)):
+        assert abs(k - n * p) < 5 * math.sqrt(n * p * (1 - p)) + 1, (K, k, n * p)
+    exp = pos.sum() / 32
+    chi2 = ((pos - exp) ** 2 / exp).sum()
+    assert chi2 < 70, chi2  # 31 dof, p ~ 1e-4
