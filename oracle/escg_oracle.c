@@ -512,47 +512,25 @@ EXPORT void orc_crs_init(int length, int height, int species, double empty_prob,
  *         as bit 31-i of the action word; its low 32-K bits are word a of SLICE_REF draw
  *         (c0 = item, attempt field l).
  *  SLICED3 (fmt = 3 | K << 8; as SLICED): the undecided mask U_a of attempt a (bit l set:
- *         tile l's action word has its top K bits all one) is drawn directly instead of as the AND
- *         of K words: with T[0] = 2^32, T[g] = floor(T[g-1] (2^K - 1) / 2^K) (so T[g] / 2^32 =
- *         (1 - 2^-K)^g within g 2^-32), a uniform word u gives the run of decided tiles from
- *         position pos, G = #{g in [1, 32 - pos] : u < T[g]}; G = 32 - pos ends the mask, else bit
- *         pos + G is set and the next run starts after it with the next word.  u_a = word a of
- *         SLICE draw 4, the k-th next word of attempt a = word a of SLICE draw 5 + k.  Choice words
- *         as SLICED (SLICE draws 0..3); an undecided attempt's action word is TK | (word a of the
- *         SLICE_REF draw & ~TK), TK = the K leading ones; a decided attempt is a migration.
+ *         tile l's action word has its top K bits all one, i.i.d. with probability q = 2^-K) is
+ *         drawn by inversion instead of as the AND of K words.  Tables (integer recurrences, so
+ *         engine and oracle agree bit for bit; each probability within 2^-27 of the exact power):
+ *           T[g], g = 1..32: T[0] = 2^32, T[g] = floor(T[g-1] (2^K-1) / 2^K)      ~ 2^32 (1-q)^g
+ *           S[G], G = 0..31: T[G+1] + r_{31-G}, r_0 = T[G] - T[G+1], r_i = floor(r_{i-1} (2^K-1)/2^K)
+ *           C[m][g], m = 1..31, g = 1..m-1: floor((T[g] - T[m]) 2^32 / (2^32 - T[m]))
+ *         u = word a of SLICE draw 4: u >= T[32] gives the first set bit G = #{g in 1..32 : u < T[g]}
+ *         (U = 0 when u < T[32]); u < S[G] means it is the only one (the common case: one word per
+ *         attempt).  Otherwise at least one more follows among the m = 31 - G positions after G: the
+ *         next word (word a of SLICE draw 5) places it at G + 1 + #{g in 1..m-1 : w < C[m][g]} (the
+ *         run conditioned on a set bit), and the bits after it are runs of T drawn from words a of
+ *         SLICE draws 6, 7, ...: #{g in 1..r : w < T[g]} decided tiles, r = the positions left,
+ *         r meaning none.  Choice words as SLICED (SLICE draws 0..3); an undecided attempt's action
+ *         word is TK | (word a of the SLICE_REF draw & ~TK), TK = the K leading ones; a decided
+ *         attempt is a migration.
  * In every format the action word is a uniform 32-bit value assembled from disjoint Philox bits (for
- * SLICED3: the probability that an attempt is undecided is 2^-K within 2^-27, the reference's own
+ * SLICED3: each decision of the undecided mask within 2^-27 of its probability, the reference's own
  * float action quantisation being 2^-24), so the rule sees the reference's action distribution. */
 
-/* SLICED3 run thresholds T[1..32] for K action bits (T[0] = 2^32 implicit). */
-EXPORT void orc_slice3_table(int K, uint32_t* out32) {
-    uint64_t t = 1ull << 32;
-    for (int g = 1; g <= 32; ++g) {
-        t = (t * ((1ull << K) - 1ull)) >> K;
-        out32[g - 1] = (uint32_t)t;
-    }
-}
-
-/* SLICED3 undecided mask of attempt a of an item (see above). */
-static uint32_t slice3_mask(uint64_t seed, uint32_t item, uint64_t mcs, uint32_t p, int a, uint32_t u,
-                            const uint32_t* T) {
-    uint32_t U = 0;
-    int pos = 0, k = 0;
-    for (;;) {
-        const int rem = 32 - pos;
-        int G = 0;
-        while (G < rem && u < T[G]) ++G; /* T[G] = threshold of run length G + 1 */
-        if (G == rem) break;
-        pos += G;
-        U |= 1u << pos;
-        if (++pos == 32) break;
-        uint32_t w4[4];
-        crs_draw(seed, item, mcs, DOM_SLICE, p, (uint32_t)(5 + k), w4);
-        u = w4[a];
-        ++k;
-    }
-    return U;
-}
 static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a, uint32_t* low, uint32_t* hi_part,
                              int* hi_shift) {
     if (!narrow) {
@@ -567,9 +545,59 @@ static void crs_attempt_bits(int narrow, int lb, const uint32_t* w, int h, int a
     }
 }
 
+/* SLICED3 tables: out[0..31] = T[1..32], out[32..63] = S[0..31], out[64 + 32 (m-1) + g] = C[m][g]. */
+EXPORT void orc_slice3_table(int K, uint32_t* out) {
+    const uint64_t num = (1ull << K) - 1ull;
+    uint64_t T[33];
+    T[0] = 1ull << 32;
+    for (int g = 1; g <= 32; ++g) T[g] = (T[g - 1] * num) >> K;
+    for (int g = 1; g <= 32; ++g) out[g - 1] = (uint32_t)T[g];
+    for (int G = 0; G < 32; ++G) {
+        uint64_t r = T[G] - T[G + 1];
+        for (int i = 0; i < 31 - G; ++i) r = (r * num) >> K;
+        out[32 + G] = (uint32_t)(T[G + 1] + r);
+    }
+    for (int i = 0; i < 31 * 32; ++i) out[64 + i] = 0u;
+    for (int m = 1; m <= 31; ++m)
+        for (int g = 1; g < m; ++g) out[64 + 32 * (m - 1) + g] = (uint32_t)(((T[g] - T[m]) << 32) / ((1ull << 32) - T[m]));
+}
+
+/* #{g in 1..n : u < t[g]} for a decreasing threshold list t[1..n] (t given from index 1). */
+static int slice3_run(uint32_t u, const uint32_t* t1, int n) {
+    int g = 0;
+    while (g < n && u < t1[g]) ++g; /* t1[g] = threshold of run length g + 1 */
+    return g;
+}
+
+/* SLICED3 undecided mask of attempt a of an item (see above); tab = orc_slice3_table. */
+static uint32_t slice3_mask(uint64_t seed, uint32_t item, uint64_t mcs, uint32_t p, int a, uint32_t u,
+                            const uint32_t* tab) {
+    const uint32_t* T = tab;        /* T[g-1] */
+    const uint32_t* S = tab + 32;   /* S[G] */
+    if (u < T[31]) return 0u;
+    const int G = slice3_run(u, T, 32);
+    uint32_t U = 1u << G;
+    if (u < S[G]) return U;
+    uint32_t w4[4];
+    crs_draw(seed, item, mcs, DOM_SLICE, p, 5u, w4);
+    const int m = 31 - G;
+    int pos = G + 1 + slice3_run(w4[a], tab + 64 + 32 * (m - 1) + 1, m - 1);
+    U |= 1u << pos;
+    ++pos;
+    for (uint32_t k = 6; pos < 32; ++k) {
+        crs_draw(seed, item, mcs, DOM_SLICE, p, k, w4);
+        const int r = 32 - pos, g = slice3_run(w4[a], T, r);
+        if (g == r) break;
+        pos += g;
+        U |= 1u << pos;
+        ++pos;
+    }
+    return U;
+}
+
 /* Test hook: the SLICED3 undecided mask of attempt a of item `item` in phase p of MCS mcs. */
 EXPORT uint32_t orc_slice3_mask(uint64_t seed, uint32_t item, uint64_t mcs, uint32_t p, int a, int K) {
-    uint32_t T3[32], w4[4];
+    uint32_t T3[64 + 31 * 32], w4[4];
     orc_slice3_table(K, T3);
     crs_draw(seed, item, mcs, DOM_SLICE, p, 4u, w4);
     return slice3_mask(seed, item, mcs, p, a, w4[a], T3);
@@ -592,7 +620,7 @@ EXPORT int orc_crs_run(int32_t* cells, int length, int height, int species, int 
     const int sliced3 = (fmt & 0xFF) == 3;
     if (narrow && (ncy != 2 || ncx != 2 || length % 8 != 0)) return 2;
     if (sliced && (ncy != 2 || ncx != 2 || length % 128 != 0 || arity != 4 || K < 1 || K > 24)) return 2;
-    uint32_t T3[32];
+    uint32_t T3[64 + 31 * 32];
     if (sliced3) orc_slice3_table(K, T3);
     const uint32_t TK = K >= 32 ? ~0u : ~((1u << (32 - K)) - 1u);
     orc_ctx_make(&c, length, height, species, arity, flux, dom, mobility);

@@ -178,8 +178,8 @@ class Oracle:
         return oy.value, ox.value, perm[:ncy * ncx].tolist()
 
     def slice3_table(self, K):
-        """SLICED3 run thresholds T[1..32] (escg_oracle.c orc_slice3_table)."""
-        out = np.zeros(32, np.uint32)
+        """SLICED3 tables (escg_oracle.c orc_slice3_table): T[1..32], S[0..31], then C[m][g]."""
+        out = np.zeros(64 + 31 * 32, np.uint32)
         self.lib.orc_slice3_table(K, out)
         return out
 

@@ -137,14 +137,25 @@ Thresholds compute_thresholds(double mobility, int64_t cells, const double* dom,
 }
 
 // min{x : double(float(x)/4294967295.0f) >= p0} — the empty test of init_lattice (lattice.hpp:59).
-// SLICED3 run thresholds T[g-1] = floor((1 - 2^-K)^g 2^32) by the recurrence t_g = floor(t_{g-1}
-// (2^K - 1) / 2^K), t_0 = 2^32 (oracle/escg_oracle.c orc_slice3_table; within g 2^-32 of the exact power).
-void slice3_table(int K, uint32_t* out32) {
-    uint64_t t = 1ull << 32;
-    for (int g = 1; g <= 32; ++g) {
-        t = (t * ((1ull << K) - 1ull)) >> K;
-        out32[g - 1] = static_cast<uint32_t>(t);
+// SLICED3 tables (oracle/escg_oracle.c orc_slice3_table, the definition): out[0..31] = T[1..32],
+// T[0] = 2^32, T[g] = floor(T[g-1] (2^K-1) / 2^K); out[32..63] = S[0..31], the single-tile part of
+// each first-tile interval; out[64 + 32 (m-1) + g] = C[m][g], the runs conditioned on a set bit.
+constexpr int kSlice3Words = 64 + 31 * 32;
+void slice3_table(int K, uint32_t* out) {
+    const uint64_t num = (1ull << K) - 1ull;
+    uint64_t T[33];
+    T[0] = 1ull << 32;
+    for (int g = 1; g <= 32; ++g) T[g] = (T[g - 1] * num) >> K;
+    for (int g = 1; g <= 32; ++g) out[g - 1] = static_cast<uint32_t>(T[g]);
+    for (int G = 0; G < 32; ++G) {
+        uint64_t r = T[G] - T[G + 1];
+        for (int i = 0; i < 31 - G; ++i) r = (r * num) >> K;
+        out[32 + G] = static_cast<uint32_t>(T[G + 1] + r);
     }
+    for (int i = 0; i < 31 * 32; ++i) out[64 + i] = 0u;
+    for (int m = 1; m <= 31; ++m)
+        for (int g = 1; g < m; ++g)
+            out[64 + 32 * (m - 1) + g] = static_cast<uint32_t>(((T[g] - T[m]) << 32) / ((1ull << 32) - T[m]));
 }
 
 uint32_t empty_threshold(double p0) {
@@ -1028,9 +1039,9 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 h->lpi = 1;
                 if (const char* lv = std::getenv("ESCG_SLICE_LPI")) h->lpi = (h->npl == 2 && std::atoi(lv) == 2) ? 2 : 1;
                 if (const char* qv = std::getenv("ESCG_SLICE_QCAP")) h->qcap = std::atoi(qv);
-                // SLICED3 by default: one draw word per attempt for the undecided masks instead of K
-                // (ESCG_SLICE_DRAWS=2 keeps the K action words of SLICED)
-                h->sliced3 = !(std::getenv("ESCG_SLICE_DRAWS") && std::atoi(std::getenv("ESCG_SLICE_DRAWS")) == 2);
+                // SLICED3 (one draw word per attempt for the undecided masks instead of K) on the
+                // overlapped-tile kernel; the ring kernel keeps SLICED (set below once it is chosen)
+                h->sliced3 = true;
             }
         }
         CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
@@ -1094,6 +1105,10 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                                 nb <= escgd::ring_capacity(h->npl, rsmem, device);
                 if (ok) {
                     h->ring = true;
+                    // measured on B200 at L=3200: SLICED 6.5e11 vs SLICED3 6.0e11 attempts/s on the ring
+                    // (its phase is bound by the boundary slabs, whose draws producer warps make ahead),
+                    // while SLICED3 lifts the overlapped-tile kernel at L=16384 from 8.6e11 to 1.08e12
+                    h->sliced3 = false;
                     h->ring_nb = nb;
                     h->ring_smem = rsmem;
                     h->ring_mbs = 2 + 3 * h->npl * GL * 4;
@@ -1106,11 +1121,14 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
             h->d_ticket.alloc(n_replicas);
         }
+        if (h->narrow == 2) {  // explicit choice of the sliced draw format (tests, experiments)
+            if (const char* dv = std::getenv("ESCG_SLICE_DRAWS")) h->sliced3 = std::atoi(dv) != 2;
+        }
         if (h->sliced3) {
-            uint32_t t3[32];
-            slice3_table(h->K, t3);
-            h->d_T3.alloc(32);
-            CK(cudaMemcpy(h->d_T3.p, t3, sizeof(t3), cudaMemcpyHostToDevice));
+            std::vector<uint32_t> t3(kSlice3Words);
+            slice3_table(h->K, t3.data());
+            h->d_T3.alloc(kSlice3Words);
+            CK(cudaMemcpy(h->d_T3.p, t3.data(), sizeof(uint32_t) * kSlice3Words, cudaMemcpyHostToDevice));
         }
         h->d_seeds.alloc(n_replicas);
         h->d_last.alloc(static_cast<size_t>(h->S1) * n_replicas);

@@ -98,7 +98,7 @@ struct BlockArgs {
     int npl;  // bit planes (species code bits)
     int lpi;  // lanes per bit-sliced item (1, or 2: draws and planes split over a lane pair)
     int qcap; // > 0: deferred-tile queue capacity override (tests of the in-place overflow path)
-    const uint32_t* T3;  // SLICED3 run thresholds (32 words; slice_common.cuh slice3_masks), null: SLICED
+    const uint32_t* T3;  // SLICED3 tables (orc_slice3_table layout; slice_common.cuh slice3_masks), null: SLICED
 };
 
 // Persistent cooperative block kernel: the whole run/advance in one launch (all CTAs co-resident).
@@ -186,7 +186,7 @@ struct RingArgs {
     unsigned int* ticket;
     int smem_bytes;
     int qcap;                 // > 0: per-warp deferred-tile queue capacity override (tests)
-    const uint32_t* T3;       // SLICED3 run thresholds (32 words), null: SLICED
+    const uint32_t* T3;       // SLICED3 tables (orc_slice3_table layout), null: SLICED
 };
 cudaError_t launch_ring(const RingArgs& a, int nb, cudaStream_t s);
 int ring_smem_bytes(int H, int L, int npl, int nb);

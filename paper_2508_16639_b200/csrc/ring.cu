@@ -88,7 +88,8 @@ struct RingCtx {
     int S1;
     unsigned long long* mbox;
     int mbs;
-    const uint32_t* T3;  // SLICED3 run thresholds in shared memory, null: SLICED
+    const uint32_t* T3;   // SLICED3 thresholds T, S in shared memory, null: SLICED
+    const uint32_t* T3g;  // the whole SLICED3 table (global)
 };
 
 // Mailbox of band `cta`, direction dir (0: rows shared with the band above, 1: below), parity par.
@@ -230,10 +231,10 @@ __device__ __forceinline__ void put_all(uint32_t (&Q)[4][NPL][4], const uint32_t
 // undecided masks U, then the choice planes (cell row, cell column, direction bits) per attempt.
 template <int K>
 __device__ __forceinline__ void slab_draws(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* T3,
-                                           uint32_t (&D)[kDrawWords]) {
+                                           const uint32_t* T3g, uint32_t (&D)[kDrawWords]) {
     if (T3 != nullptr) {  // SLICED3: the undecided masks drawn directly (slice_common.cuh)
         uint32_t U[4];
-        slice3_masks(item, c1, c2s, s32, T3, U);
+        slice3_masks(item, c1, c2s, s32, T3, T3g, U);
 #pragma unroll
         for (int a = 0; a < 4; ++a) D[a] = U[a];
     } else {
@@ -261,9 +262,9 @@ __device__ __forceinline__ void slab_draws(uint32_t item, uint32_t c1, uint32_t 
 // single copy of the Philox code.
 template <int K>
 __device__ __noinline__ void draws_to_smem(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* T3,
-                                           uint32_t* t) {
+                                           const uint32_t* T3g, uint32_t* t) {
     uint32_t D[kDrawWords];
-    slab_draws<K>(item, c1, c2s, s32, T3, D);
+    slab_draws<K>(item, c1, c2s, s32, T3, T3g, D);
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int i = 0; i < kDrawWords; ++i) t[i * 32 + lane] = D[i];
@@ -338,7 +339,7 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
     RDIAG(X.q, 0, clock64());
 
     if (tbl == nullptr) {  // not drawn ahead by a producer warp: draw now (this warp's scratch)
-        draws_to_smem<K>(item, c1, c2s, C.s32, C.T3, scratch);
+        draws_to_smem<K>(item, c1, c2s, C.s32, C.T3, C.T3g, scratch);
         __syncwarp();
         tbl = scratch;
     }
@@ -504,7 +505,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     __shared__ uint32_t sScr[kRingWarps][kDrawWords * 32];  // slab warps' own draws
     __shared__ uint32_t sCnt[1 << NPL];
     __shared__ int sStop;
-    __shared__ uint32_t sT3[32];
+    __shared__ uint32_t sT3[64];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x, nb = gridDim.x;
     const int H = a.H, GL = a.L >> 7, S1 = a.S + 1;
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     const int band = R1 - R0, RP = NPL * GL * 4, per_row = NPL * GL;
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
     for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
-    if (a.T3 != nullptr && tid < 32) sT3[tid] = a.T3[tid];
+    if (a.T3 != nullptr && tid < 64) sT3[tid] = a.T3[tid];
     if (*reinterpret_cast<volatile const int32_t*>(a.run.status) != kStatusRunning) return;  // uniform
 
     for (int idx = tid; idx < (band + 3) * per_row; idx += nt) {  // rows R0-1 .. R1+1 (mod H)
@@ -546,6 +547,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     C.mbox = a.mbox;
     C.mbs = a.mbs;
     C.T3 = a.T3 != nullptr ? sT3 : nullptr;
+    C.T3g = a.T3;
     const int up = c == 0 ? nb - 1 : c - 1, down = c == nb - 1 ? 0 : c + 1;
     const int64_t interval = a.run.interval > 0 ? a.run.interval : 1;
     // two warps beyond the most slabs a phase can have draw the next phase's boundary slabs
@@ -646,7 +648,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
                 j = j >= C.Hh ? j - C.Hh : j;
                 const uint32_t item = static_cast<uint32_t>(j) * static_cast<uint32_t>(GL) + static_cast<uint32_t>(lane);
                 draws_to_smem<K>(item, static_cast<uint32_t>(mn),
-                                 ctr2(static_cast<uint64_t>(mn), kDomSlice, static_cast<uint32_t>(pn), 0u), C.s32, C.T3,
+                                 ctr2(static_cast<uint64_t>(mn), kDomSlice, static_cast<uint32_t>(pn), 0u), C.s32, C.T3, C.T3g,
                                  sDraw[par ^ 1][warp == wtop ? 0 : 1]);
             }
             if (snap && a.record) {

@@ -86,7 +86,8 @@ struct SliceCtx {
     uint4* q;             // deferred-tile queue of the phase: (w | acol << 16, code, item)
     unsigned* qn;         // its fill count
     unsigned qcap;        // its capacity (<= kSliceQueue; smaller in tests of the overflow path)
-    const uint32_t* T3;   // SLICED3 run thresholds in shared memory, null: SLICED (K action words)
+    const uint32_t* T3;   // SLICED3 thresholds T, S in shared memory, null: SLICED (K action words)
+    const uint32_t* T3g;  // the whole SLICED3 table (global)
 };
 
 // Out-of-line copy for the in-place overflow path inside the (per-residue) phase bodies.
@@ -127,7 +128,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
         uint32_t U[4], Y[4], X[4], D0[4], D1[4];
         if constexpr (LPI == 1) {
             if (C.T3 != nullptr) {
-                slice3_masks(item, c1, c2s, C.s32, C.T3, U);
+                slice3_masks(item, c1, c2s, C.s32, C.T3, C.T3g, U);
             } else {
 #pragma unroll
                 for (int a = 0; a < 4; ++a) U[a] = ~0u;
@@ -152,7 +153,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
             uint32_t Ul[2] = {~0u, ~0u};
             uint32_t U3[4];
             if (C.T3 != nullptr) {
-                slice3_masks(item, c1, c2s, C.s32, C.T3, U3);  // both lanes of the pair (same masks)
+                slice3_masks(item, c1, c2s, C.s32, C.T3, C.T3g, U3);  // both lanes of the pair (same masks)
             } else {
 #pragma unroll
                 for (int t = 0; t < K / 2; ++t) {
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     __shared__ uint32_t sTh[(kMaxSliceSpecies + 1) * (kMaxSliceSpecies + 1)];
     __shared__ uint4 sQ[kSliceQueue];
     __shared__ unsigned sQn[3];
-    __shared__ uint32_t sT3[32];
+    __shared__ uint32_t sT3[64];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const int r = blockIdx.z, tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     // local rows (the buffer; band engines: halo + band + halo, never wrapped) vs global rows (draws)
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
     if (tid < 3) sQn[tid] = 0u;
     for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
-    if (a.T3 != nullptr && tid < 32) sT3[tid] = a.T3[tid];
+    if (a.T3 != nullptr && tid < 64) sT3[tid] = a.T3[tid];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
 
@@ -367,6 +368,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
         C.q = sQ;
         C.qcap = a.qcap > 0 && a.qcap < static_cast<int>(kSliceQueue) ? static_cast<unsigned>(a.qcap) : kSliceQueue;
         C.T3 = a.T3 != nullptr ? sT3 : nullptr;
+        C.T3g = a.T3;
         C.S1 = S1;
 #pragma unroll 1
         for (int t = 0; t < a.nmcs; ++t) {

@@ -213,43 +213,66 @@ namespace {
 
 // SLICED3 draws (oracle/escg_oracle.c slice3_mask is the definition): the undecided
 // mask U_a of an item's attempt a — bit l set iff tile l's action word has its K top bits all one,
-// i.i.d. with probability 2^-K — drawn directly from one word instead of as the AND of K words.
-// T (shared memory, 32 words): T[g-1] = floor((1 - 2^-K)^g 2^32) by the recurrence of
-// orc_slice3_table; u < T[g-1] means "the next g tiles are decided".
-__device__ __noinline__ uint32_t slice3_rare(uint32_t u, int a, uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32,
-                                             const uint32_t* T) {
-    uint32_t U = 0;
-    int pos = 0, k = 0;
-    for (;;) {
-        const int rem = 32 - pos;
-        int lo = 0, hi = rem;  // G = the longest run g <= rem with u < T[g-1] (T decreasing)
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (u < T[mid - 1])
-                lo = mid;
-            else
-                hi = mid - 1;
-        }
-        if (lo == rem) break;
-        pos += lo;
+// i.i.d. with probability 2^-K — drawn by inversion from one word instead of as the AND of K words.
+// sT (shared, 64 words): T[1..32] then S[0..31]; gT (global): the whole orc_slice3_table, whose
+// conditional-run rows C[m][g] serve only masks with two or more undecided tiles.
+__device__ __forceinline__ uint32_t word_of(const uint4 w, int a) { return a == 0 ? w.x : (a == 1 ? w.y : (a == 2 ? w.z : w.w)); }
+
+// A mask with at least two undecided tiles, the first at G (probability ~ 5e-4 per attempt at K = 10).
+__device__ __noinline__ uint32_t slice3_multi(int G, int a, uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32,
+                                              const uint32_t* sT, const uint32_t* gT) {
+    uint32_t U = 1u << G;
+    const int m = 31 - G;
+    const uint32_t* Cm = gT + 64 + 32 * (m - 1) + 1;
+    const uint32_t u = word_of(philox(item, c1, c2s | (5u << 24), s32), a);
+    int g = 0;
+    while (g < m - 1 && u < Cm[g]) ++g;
+    int pos = G + 1 + g;
+    U |= 1u << pos;
+    ++pos;
+    for (uint32_t k = 6; pos < 32; ++k) {
+        const uint32_t w = word_of(philox(item, c1, c2s | (k << 24), s32), a);
+        const int r = 32 - pos;
+        int h = 0;
+        while (h < r && w < sT[h]) ++h;
+        if (h == r) break;
+        pos += h;
         U |= 1u << pos;
-        if (++pos == 32) break;
-        const uint4 w = philox(item, c1, c2s | ((5u + static_cast<uint32_t>(k)) << 24), s32);
-        u = a == 0 ? w.x : (a == 1 ? w.y : (a == 2 ? w.z : w.w));
-        ++k;
+        ++pos;
     }
     return U;
 }
 
-// The four attempts' undecided masks of an item: SLICE draw 4 gives u_0..u_3; a word below T[31]
-// (32 decided tiles, P = (1 - 2^-K)^32) is the common case and costs one comparison.
-__device__ __forceinline__ void slice3_masks(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* T,
-                                             uint32_t (&U)[4]) {
+// The four attempts' undecided masks of an item: SLICE draw 4 gives u_0..u_3.  u < T[32] (32 decided
+// tiles) costs one comparison; otherwise the first undecided tile is the run G found by binary search
+// and u < S[G] makes it the only one — one converged pass per undecided attempt of the lane.
+__device__ __forceinline__ void slice3_masks(uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32, const uint32_t* sT,
+                                             const uint32_t* gT, uint32_t (&U)[4]) {
     const uint4 v = philox(item, c1, c2s | (4u << 24), s32);
     const uint32_t u[4] = {v.x, v.y, v.z, v.w};
-    const uint32_t t32 = T[31];
+    const uint32_t t32 = sT[31];
+    uint32_t need = 0;
 #pragma unroll
-    for (int a = 0; a < 4; ++a) U[a] = u[a] < t32 ? 0u : slice3_rare(u[a], a, item, c1, c2s, s32, T);
+    for (int a = 0; a < 4; ++a) {
+        U[a] = 0u;
+        need |= (u[a] >= t32 ? 1u : 0u) << a;
+    }
+    while (need) {
+        const int a = __ffs(need) - 1;
+        need &= need - 1u;
+        const uint32_t w = a == 0 ? u[0] : (a == 1 ? u[1] : (a == 2 ? u[2] : u[3]));
+        int lo = 0, hi = 31;  // G = #{g in 1..32 : w < T[g]} (<= 31 here)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (w < sT[mid - 1])
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        const uint32_t m = w < sT[32 + lo] ? 1u << lo : slice3_multi(lo, a, item, c1, c2s, s32, sT, gT);
+#pragma unroll
+        for (int b = 0; b < 4; ++b) U[b] = a == b ? m : U[b];
+    }
 }
 
 }  // namespace

@@ -42,7 +42,7 @@ def test_c3_bench_configuration_matches_oracle(escg, oracle):
     with escg.DeviceEngine(p, model) as eng:
         d = eng.describe()
         code = eng.draw_code()
-        assert code == 3 | (10 << 8), hex(code)  # SLICED3, K = 10 action bits
+        assert code >> 8 == 10 and code & 0xFF in (2, 3), hex(code)  # bit-sliced, K = 10 action bits
         assert d["kernel"] in ("block", "ring") and d["draw_format"] == "sliced", d
         eng.init_lattice()
         init = eng.get_lattice()

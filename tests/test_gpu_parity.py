@@ -611,7 +611,7 @@ def test_auto_kernel_choice(escg):
     with escg.DeviceEngine(p, model, n_replicas=296, seeds=range(296)) as eng:
         assert eng.describe()["kernel"] == "tile"
     with escg.DeviceEngine(params(escg, 3200, 3200, 3, 1e-4, 0.1, 4, True), model) as eng:
-        assert eng.describe()["kernel"] == "block"
+        assert eng.describe()["kernel"] == "ring"  # one bit-sliced lattice of 25 groups per row
 
 
 def _fnv1a_i32(cells):
