@@ -114,6 +114,7 @@ __device__ __forceinline__ void ring_publish(const RingCtx& C, int dir, int wrow
             for (int p = 0; p < NPL; ++p) {
                 const uint4 v = lds128(C.sw + (wrow0 + s) * C.RP + (p * C.GL + lane) * 4);
                 unsigned long long* d = mb + mslot<NPL>(C, s, p, lane);
+                ESCG_CHECK(s >= 0 && s < 3 && mslot<NPL>(C, s, p, lane) + 3 < C.mbs && wrow0 + s <= C.R1 - C.R0 + 2);
                 st_tag2(d, v.x, v.y, tag);
                 st_tag2(d + 2, v.z, v.w, tag);
             }
@@ -333,6 +334,7 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
     const int lane = threadIdx.x & 31;
     const bool valid = lane < C.GL;
     const int wl = w - C.R0 + 1;  // window row of the anchor
+    ESCG_CHECK(wl >= 1 && wl + 2 <= C.R1 - C.R0 + 2 && C.GL <= 32);
     int j = (w + oy) >> 1;
     j = j >= C.Hh ? j - C.Hh : j;
     const uint32_t item = static_cast<uint32_t>(j) * static_cast<uint32_t>(C.GL) + static_cast<uint32_t>(lane);
@@ -459,6 +461,7 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
         for (int rr = 0; rr < 4; ++rr) {
             int gy = w - 1 + rr;
             gy = gy < 0 ? gy + C.H : (gy >= C.H ? gy - C.H : gy);
+            ESCG_CHECK(gy >= 0 && gy < C.H);
 #pragma unroll
             for (int p = 0; p < NPL; ++p)
                 __stcg(reinterpret_cast<uint4*>(dst + ((static_cast<size_t>(gy) * NPL + p) * C.GL + lane) * 4),

@@ -88,6 +88,7 @@ struct SliceCtx {
     unsigned qcap;        // its capacity (<= kSliceQueue; smaller in tests of the overflow path)
     const uint32_t* T3;   // SLICED3 thresholds T, S in shared memory, null: SLICED (K action words)
     const uint32_t* T3g;  // the whole SLICED3 table (global)
+    int Wh;               // window rows (checked builds)
 };
 
 // Out-of-line copy for the in-place overflow path inside the (per-residue) phase bodies.
@@ -183,6 +184,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
 
         // footprint rows w-1 .. w+2 of this group (this lane's planes)
         uint32_t Q[4][NP][4];
+        ESCG_CHECK(!valid || (w >= 1 && w + 2 < C.Wh && C.gw < C.Gw));
         uint32_t* rowp = C.sw + (valid ? w - 1 : 0) * C.RP + C.gw * 4 + h * NP * C.Gw * 4;
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
@@ -275,6 +277,7 @@ __device__ __forceinline__ void slice_phase(const SliceCtx& C, int oy, int yr, i
             const int acol = 128 * C.gw + 4 * l + XR;
             const unsigned slot = atomicAdd(C.qn, 1u);
             if (slot < C.qcap) {
+                ESCG_CHECK(slot < kSliceQueue);
                 C.q[slot] = make_uint4(static_cast<uint32_t>(w) | (static_cast<uint32_t>(acol) << 16), code, item, 0u);
             } else {  // queue full: replay in place (the tile's footprint is disjoint from every other)
                 slice_replay_ool<NPL>(C.sw0, C.RP, C.Gw, w, acol, code, item, l, c1, c2r, C.s32, C.xm, C.xi, C.TK, C.sT,
@@ -369,6 +372,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
         C.qcap = a.qcap > 0 && a.qcap < static_cast<int>(kSliceQueue) ? static_cast<unsigned>(a.qcap) : kSliceQueue;
         C.T3 = a.T3 != nullptr ? sT3 : nullptr;
         C.T3g = a.T3;
+        C.Wh = Wh;
         C.S1 = S1;
 #pragma unroll 1
         for (int t = 0; t < a.nmcs; ++t) {

@@ -8,6 +8,16 @@
 
 #include "crs.cuh"
 
+// Checked builds (ESCG_CHECKED; tools/sanitize_cases.py — compute-sanitizer is closed on this pool):
+// device asserts on shared-memory window rows and columns, queue and mailbox slots, snapshot rows.
+#ifdef ESCG_CHECKED
+#undef NDEBUG
+#include <cassert>
+#define ESCG_CHECK(c) assert(c)
+#else
+#define ESCG_CHECK(c) ((void)0)
+#endif
+
 namespace escgd {
 namespace {
 
@@ -73,6 +83,7 @@ __device__ __forceinline__ void slice_replay(uint32_t sw0, int RP, int Gw, int w
         const int row = w - 1 + kRow[k];
         int col = acol - 1 + kCol[k];
         if (Wc) col = col < 0 ? col + Wc : (col >= Wc ? col - Wc : col);  // full-width rows wrap
+        ESCG_CHECK(row >= 0 && col >= 0 && col < 128 * Gw);
         addr[k] = sw0 + 4u * static_cast<uint32_t>(row * RP + (col >> 7) * 4 + (col & 3));
         bit[k] = (static_cast<uint32_t>(col) >> 2) & 31u;
         uint32_t v = 0;
@@ -151,6 +162,7 @@ __device__ __forceinline__ void slice_replay_group(uint32_t sw0, int RP, int Gw,
             const int row = w - 1 + rr;
             int col = acol - 1 + cc;
             if (Wc) col = col < 0 ? col + Wc : (col >= Wc ? col - Wc : col);
+            ESCG_CHECK(row >= 0 && col >= 0 && col < 128 * Gw);
             addr[t] = sw0 + 4u * static_cast<uint32_t>(row * RP + (col >> 7) * 4 + (col & 3));
             bit[t] = (static_cast<uint32_t>(col) >> 2) & 31u;
             uint32_t v = 0;

@@ -1,6 +1,8 @@
-"""Small runs of every kernel for compute-sanitizer (racecheck / memcheck / synccheck):
+"""Small runs of every kernel, each checked bit for bit against the oracle — under a checked build
+(ESCG_CHECKED: device asserts on window rows/columns, queue and mailbox slots, snapshot rows) since
+compute-sanitizer is closed on this pool:
 
-    compute-sanitizer --tool racecheck python tools/sanitize_cases.py <case>
+    ESCG_LIB=tools/_checked.so python tools/sanitize_cases.py all
 cases: tile, block, block_seam, block_reflect, slice, slice_qcap, slice_lpi2, ring, ring_stop, all
 Each case runs a few MCS on a small lattice through the C ABI and checks the result against the oracle
 (so a sanitizer-perturbed schedule would also show as a mismatch)."""
