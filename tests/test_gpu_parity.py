@@ -753,3 +753,35 @@ def test_slice_kernel_replicas_and_stops(escg, oracle, monkeypatch):
         st = eng.run(9, interval=3, tracked=2)
         assert int(st[0]) == int(escg.RunStatus.Stopped) and eng.mcs() == 0
         assert np.array_equal(eng.get_lattice(), cells)
+
+
+@pytest.mark.parametrize("L,H,kmcs", [(4480, 3364, 2), (16384, 1024, 2), (1024, 512, 1)])
+def test_band_engines_keep_their_chunk(escg, L, H, kmcs):
+    """Band engines run exactly the chunk (halo depth) they were created with — the planner searches
+    only the split — so every band of a lattice exchanges halos at the same cadence (ADVICE r01:
+    4480 x 3364 in 2 bands used to plan k=2 and k=1 for its two bands)."""
+    from paper_2508_16639_b200 import bands
+
+    p = escg.SimParams(length=L, height=H, species=3, mobility=1e-4, empty_prob=0.1, seed=3, mcs_limit=10)
+    with bands.BandGroup(p, escg.make_circulant(3, [1]), 2, kmcs=kmcs) as g:
+        assert [i["kmcs"] for i in g.info] == [kmcs, kmcs], g.info
+        assert [i["halo"] for i in g.info] == [12 * kmcs, 12 * kmcs], g.info
+
+
+def test_simulate_reuses_engine_with_new_seed(escg, oracle):
+    """escg_simulate caches its engine by shape, model and environment, not by seed: a new seed on
+    the cached engine gives that seed's run (equal to a fresh engine's), and the old seed again
+    reproduces the first result."""
+    L = 128
+    p1 = escg.SimParams(length=L, height=L, species=3, mobility=1e-3, empty_prob=0.1, seed=11, mcs_limit=30)
+    p2 = escg.SimParams(length=L, height=L, species=3, mobility=1e-3, empty_prob=0.1, seed=12, mcs_limit=30)
+    model = escg.make_circulant(3, [1])
+    r1 = escg.simulate(p1, model, escg.EngineMode.Serial).state.lattice.cells
+    r2 = escg.simulate(p2, model, escg.EngineMode.Serial).state.lattice.cells
+    r1b = escg.simulate(p1, model, escg.EngineMode.Serial).state.lattice.cells
+    assert not np.array_equal(r1, r2)
+    assert np.array_equal(r1, r1b)
+    with escg.DeviceEngine(p2, model) as eng:
+        eng.init_lattice()
+        eng.run(30, interval=1)
+        assert np.array_equal(eng.get_lattice(), r2)

@@ -123,10 +123,13 @@ def test_ring_stasis_at_first_record(escg, monkeypatch):
         assert np.array_equal(eng.get_lattice(), cells)
 
 
-def test_ring_long_run_equals_block_slice_kernel(escg, monkeypatch):
+@pytest.mark.parametrize("draws", ["2", "3"])
+def test_ring_long_run_equals_block_slice_kernel(escg, monkeypatch, draws):
     """200 MCS with 9-MCS records at the bench's row width: the ring kernel and the overlapped-tile
-    bit-sliced kernel (both the oracle's schedule) give the same trace and lattice."""
+    bit-sliced kernel (both the oracle's schedule) give the same trace and lattice, for either
+    sliced draw format (each kernel's default differs, so the format is pinned here)."""
     monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    monkeypatch.setenv("ESCG_SLICE_DRAWS", draws)
     L, H, M, seed = 3200, 256, 1e-4, 77
     model = escg.make_circulant(3, [1])
     out = []
