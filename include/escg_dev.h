@@ -180,6 +180,13 @@ ESCG_API int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_
  * current rows.  Synchronous. */
 ESCG_API int escg_dev_band_step(escg_dev* h, int32_t n_mcs);
 
+/* Issue the engine's work on a caller's CUDA stream (a cudaStream_t; NULL: the engine's own stream).
+ * On a caller's stream escg_dev_band_rows / escg_dev_band_step do not synchronise the host: a band
+ * step is enqueued after, and before, the caller's halo exchange on that stream (device-ordered
+ * stepping, bands.DistributedBand).  Replaces the host synchronisation per chunk of SURVEY §8e's
+ * exchange loop; the reference's counterpart is the refill/step overlap of engine.cpp:142-162. */
+ESCG_API int escg_dev_set_stream(escg_dev* h, void* stream);
+
 /* One-call mirror of escg::simulate(params, model, mode, …) (engine.cpp:194-240) for a single
  * lattice: initialise on device (or resume from resume_cells at resume_mcs), run to completion
  * under `mode`'s record cadence with the device stop predicates, return the final int32 lattice,

@@ -46,7 +46,7 @@ EXPORTS = [
     "escg_dev_get_lattice", "escg_dev_counts", "escg_dev_advance", "escg_dev_run", "escg_dev_read_trace",
     "escg_dev_replica_result", "escg_dev_replay", "escg_dev_last_timing", "escg_dev_describe",
     "escg_dev_draw_format", "escg_dev_block_mode", "escg_simulate", "escg_dev_create_band", "escg_dev_band_info",
-    "escg_group_advance", "escg_dev_band_rows", "escg_dev_band_step",
+    "escg_group_advance", "escg_dev_band_rows", "escg_dev_band_step", "escg_dev_set_stream",
 ]
 
 _lib = None
@@ -103,6 +103,7 @@ def lib():
     _pp = C.POINTER(C.c_void_p)
     L.escg_dev_band_rows.argtypes = [_H, _pp, _pp, _pp, _pp, C.POINTER(C.c_int64)]
     L.escg_dev_band_step.argtypes = [_H, C.c_int32]
+    L.escg_dev_set_stream.argtypes = [_H, C.c_void_p]
     L.escg_simulate.argtypes = [_P, _f64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
                                 C.c_uint32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
                                 C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]

@@ -123,6 +123,14 @@ def exchange_halos(recv_top, send_top, send_bot, recv_bot, rank: int, world: int
             req.wait()
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 class _DevView:
     """Zero-copy view of engine-owned device bytes for torch (__cuda_array_interface__)."""
 
@@ -137,7 +145,9 @@ class DistributedBand:
     Each chunk of kmcs MCS: halo rows move between ring neighbours with NCCL send/recv straight
     from/to the engine's device buffers (exchange_halos), then the block kernel runs on the band
     (escg_dev_band_step).  Draws depend only on global coordinates, so the sharded run equals the
-    single-lattice run bit for bit."""
+    single-lattice run bit for bit.  The engine issues its work on torch's current stream of the
+    device (escg_dev_set_stream), so exchange and step are ordered on the device with no host
+    synchronisation per chunk (the NCCL requests make that stream wait on their own)."""
 
     def __init__(self, params: SimParams, model: DominanceModel, rank: int, world: int, device: int = 0, kmcs: int = 2,
                  group=None):
@@ -152,6 +162,15 @@ class DistributedBand:
                                          int(kmcs), C.byref(h)))
         self._h = h
         self.info = BandGroup._band_info(h)
+        self._stream = None
+        try:
+            import torch
+
+            if torch.cuda.is_available():
+                self._stream = torch.cuda.current_stream(device)
+                check(lib().escg_dev_set_stream(h, C.c_void_p(self._stream.cuda_stream)))
+        except ImportError:
+            pass
         if self.info["kmcs"] != kmcs:
             raise EngineError("band engine runs %d MCS per chunk, %d requested" % (self.info["kmcs"], kmcs))
         self._check_uniform_chunk()
@@ -214,13 +233,15 @@ class DistributedBand:
         return tuple(torch.as_tensor(_DevView(x.value, nbytes.value), device=dev) for x in p)
 
     def advance(self, n_mcs: int):
+        """Enqueue n_mcs MCS (chunks of kmcs: halo exchange, band step) on the band's stream; returns
+        without waiting for the device (synchronize the stream, or read the band, to wait)."""
         import torch
 
         k = self.info["kmcs"]
         done = 0
-        while done < n_mcs:
-            chunk = min(k, n_mcs - done)
-            exchange_halos(*self.halo_views(), self.rank, self.world, self.group)
-            torch.cuda.synchronize(self.device)  # NCCL's stream → the engine's stream
-            check(lib().escg_dev_band_step(self._h, int(chunk)))
-            done += chunk
+        with torch.cuda.stream(self._stream) if self._stream is not None else _nullctx():
+            while done < n_mcs:
+                chunk = min(k, n_mcs - done)
+                exchange_halos(*self.halo_views(), self.rank, self.world, self.group)
+                check(lib().escg_dev_band_step(self._h, int(chunk)))
+                done += chunk

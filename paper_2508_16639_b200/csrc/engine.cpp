@@ -225,6 +225,7 @@ struct escg_dev {
     int nbands = 1, band = 0, band_start = 0, band_rows = 0, halo = 0;
     int rows_begin = 0, rows_count = 0;  // rows of the local buffer the engine owns (blocks, I/O)
     cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;  // the engine's stream; `stream` may be a caller's (escg_dev_set_stream)
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev_poll = nullptr;
     int32_t* h_status = nullptr;  // pinned, status polling of the block path
     Thresholds th;
@@ -259,7 +260,7 @@ struct escg_dev {
         if (ev_poll) cudaEventDestroy(ev_poll);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
-        if (stream) cudaStreamDestroy(stream);
+        if (own_stream) cudaStreamDestroy(own_stream);
     }
 };
 
@@ -1044,7 +1045,8 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 h->sliced3 = true;
             }
         }
-        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&h->own_stream, cudaStreamNonBlocking));
+        h->stream = h->own_stream;
         CK(cudaEventCreate(&h->ev0));
         CK(cudaEventCreate(&h->ev1));
         CK(cudaEventCreateWithFlags(&h->ev_poll, cudaEventDisableTiming));
@@ -1604,7 +1606,7 @@ int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint
         size_t row = static_cast<size_t>(h->L);
         if (h->narrow == 2) {  // bit-sliced: halos move as plane rows (NPL x L/128 x 16 bytes)
             band_sync_planes(h);
-            CK(cudaStreamSynchronize(h->stream));
+            if (h->stream == h->own_stream) CK(cudaStreamSynchronize(h->stream));
             base = reinterpret_cast<uint8_t*>(h->pl[h->cur[0]].p);
             row = static_cast<size_t>(h->npl) * (h->L / 128) * 16;
         }
@@ -1667,10 +1669,22 @@ int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
         } else {
             CK(escgd::launch_block(a, 1, h->threads, h->stream));
         }
-        CK(cudaStreamSynchronize(h->stream));
+        // on the engine's own stream the step completes before return; on a caller's stream it is
+        // only enqueued, ordered after (and before) the caller's halo exchange on that stream
+        if (h->stream == h->own_stream) CK(cudaStreamSynchronize(h->stream));
+        CK(cudaGetLastError());
         h->cur[0] = 1 - par;
         h->mcs[0] += n_mcs;
         h->last_launches = 1;
+    });
+}
+
+int escg_dev_set_stream(escg_dev* h, void* stream) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        CK(cudaSetDevice(h->device));
+        CK(cudaStreamSynchronize(h->stream));  // work already enqueued on the previous stream
+        h->stream = stream ? static_cast<cudaStream_t>(stream) : h->own_stream;
     });
 }
 

@@ -785,3 +785,49 @@ def test_simulate_reuses_engine_with_new_seed(escg, oracle):
         eng.init_lattice()
         eng.run(30, interval=1)
         assert np.array_equal(eng.get_lattice(), r2)
+
+
+@pytest.mark.parametrize("fmt", ["narrow", "sliced"])
+def test_band_steps_ordered_on_the_caller_stream(escg, fmt, monkeypatch):
+    """Device-ordered band stepping (escg_dev_set_stream, what bands.DistributedBand does with NCCL):
+    halo copies and band steps enqueued on one torch stream with no host synchronisation between
+    them give the single-lattice run bit for bit."""
+    import torch
+
+    from paper_2508_16639_b200._lib import check, lib
+    from paper_2508_16639_b200.bands import DistributedBand
+
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", fmt)
+    L, H, n_bands, kmcs, T = 1024, 256, 3, 2, 9
+    p = params(escg, L, H, 3, 5e-2, 0.1, 4, True, seed=41)
+    model = escg.make_circulant(3, [1])
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        assert eng.draw_format() == fmt
+        eng.init_lattice()
+        init = eng.get_lattice()
+        eng.advance(T)
+        want = eng.get_lattice()
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        bands = [DistributedBand(p, model, rank=g, world=n_bands, device=0, kmcs=kmcs) for g in range(n_bands)]
+    try:
+        for b in bands:
+            s, r = b.info["start"], b.info["rows"]
+            b.set_band(init[s * L:(s + r) * L], 0)
+        with torch.cuda.stream(stream):
+            done = 0
+            while done < T:
+                chunk = min(kmcs, T - done)
+                views = [b.halo_views() for b in bands]
+                for g in range(n_bands):
+                    up, dn = views[(g - 1) % n_bands], views[(g + 1) % n_bands]
+                    views[g][0].copy_(up[2])
+                    views[g][3].copy_(dn[1])
+                for b in bands:
+                    check(lib().escg_dev_band_step(b._h, chunk))
+                done += chunk
+        got = np.concatenate([b.get_band() for b in bands])
+        assert np.array_equal(got, want)
+    finally:
+        for b in bands:
+            b.close()
