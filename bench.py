@@ -49,7 +49,7 @@ CONFIGS = {
                cpu_maxstep_mcs=200, cpu_serial_mcs=50, ref_step_mcs=20, published=None,
                desc="RPSLS C(5,{1,2}) L=1000 M=3e-5 p0=0 VN4 periodic, one lattice, MaxStep record cadence (100 MCS)",
                published_ref=None),
-    "C5": dict(L=16384, S=3, model="rps", M=1e-4, p0=0.1, num_randoms=5 * 16384 * 16384, mcs_per_step=20,
+    "C5": dict(L=16384, S=3, model="rps", M=1e-4, p0=0.1, num_randoms=5 * 16384 * 16384, mcs_per_step=100,
                cpu_maxstep_mcs=2, cpu_serial_mcs=None, ref_step_mcs=1, published=None,
                desc="RPS C(3,{1}) L=16384 M=1e-4 p0=0.1 VN4 periodic (268M cells), MaxStep record cadence with "
                     "numRandoms = 5N (5 MCS)",
