@@ -187,6 +187,33 @@ ESCG_API int escg_dev_band_step(escg_dev* h, int32_t n_mcs);
  * exchange loop; the reference's counterpart is the refill/step overlap of engine.cpp:142-162. */
 ESCG_API int escg_dev_set_stream(escg_dev* h, void* stream);
 
+/* Multi-part ring (the reference's row split of engine.cpp:119-131 across GPUs): part
+ * `part` of `n_parts` (2..8; rows split at multiples of 4, >= 8 rows each) of one bit-sliced
+ * lattice runs the persistent ring kernel over n_ctas bands of its rows (0: one per SM).  Its
+ * boundary bands exchange rows with the neighbouring parts inside the kernel, every colour phase,
+ * by system-scope tagged stores into the neighbour's inbox (NVLink peer memory on another GPU) —
+ * no host step, no copy kernel.  State stays in bit planes; set/get/counts address the part's rows.
+ * Wiring: escg_dev_ring_part_export gives the part's plane buffers, inbox and row count (and, if
+ * `ipc` is not NULL, 3 x 64 bytes of cudaIpcMemHandle_t for planes 0, planes 1 and the mailbox
+ * allocation, the inbox at *inbox_offset bytes into it); escg_dev_ring_part_connect takes the part
+ * above's and below's (pointers valid on this part's device: same device, peer access, or
+ * escg_ipc_open).  Then either escg_ring_group_advance over all parts from one process (one
+ * device: ONE cooperative launch over every part — the single-GPU form of the multi-GPU kernel;
+ * several devices: one launch per part, peer access enabled), or escg_dev_advance on each rank's
+ * part (one process per GPU; the launches meet through their inbox words, the host does not wait).
+ * set_lattice / init_lattice must be called on every part before the next advance of any. */
+ESCG_API int escg_dev_create_ring_part(const escg_params* p, const double* dominance, int32_t species, int32_t kind,
+                                       int32_t device, int32_t n_parts, int32_t part, int32_t n_ctas, escg_dev** out);
+ESCG_API int escg_dev_ring_part_export(escg_dev* h, void** planes0, void** planes1, void** inbox, int32_t* rows,
+                                       void* ipc, int64_t* inbox_offset);
+ESCG_API int escg_dev_ring_part_connect(escg_dev* h, void* up_planes0, void* up_planes1, void* up_inbox,
+                                        int32_t up_rows, void* dn_planes0, void* dn_planes1, void* dn_inbox,
+                                        int32_t dn_rows);
+ESCG_API int escg_ring_group_advance(escg_dev** parts, int32_t n, int64_t n_mcs);
+/* CUDA IPC (one process per GPU): open a peer's 64-byte allocation handle on `device` / close it. */
+ESCG_API int escg_ipc_open(int32_t device, const void* handle, void** ptr);
+ESCG_API int escg_ipc_close(int32_t device, void* ptr);
+
 /* One-call mirror of escg::simulate(params, model, mode, …) (engine.cpp:194-240) for a single
  * lattice: initialise on device (or resume from resume_cells at resume_mcs), run to completion
  * under `mode`'s record cadence with the device stop predicates, return the final int32 lattice,

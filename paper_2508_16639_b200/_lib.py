@@ -47,6 +47,8 @@ EXPORTS = [
     "escg_dev_replica_result", "escg_dev_replay", "escg_dev_last_timing", "escg_dev_describe",
     "escg_dev_draw_format", "escg_dev_block_mode", "escg_simulate", "escg_dev_create_band", "escg_dev_band_info",
     "escg_group_advance", "escg_dev_band_rows", "escg_dev_band_step", "escg_dev_set_stream",
+    "escg_dev_create_ring_part", "escg_dev_ring_part_export", "escg_dev_ring_part_connect", "escg_ring_group_advance",
+    "escg_ipc_open", "escg_ipc_close",
 ]
 
 _lib = None
@@ -104,11 +106,21 @@ def lib():
     L.escg_dev_band_rows.argtypes = [_H, _pp, _pp, _pp, _pp, C.POINTER(C.c_int64)]
     L.escg_dev_band_step.argtypes = [_H, C.c_int32]
     L.escg_dev_set_stream.argtypes = [_H, C.c_void_p]
+    if hasattr(L, "escg_dev_create_ring_part"):  # (diagnostic builds of older sources lack the multi-part ring)
+        L.escg_dev_create_ring_part.argtypes = [_P, _f64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                C.c_int32, C.POINTER(_H)]
+        L.escg_dev_ring_part_export.argtypes = [_H, _pp, _pp, _pp, C.POINTER(C.c_int32), C.c_void_p,
+                                                C.POINTER(C.c_int64)]
+        L.escg_dev_ring_part_connect.argtypes = [_H, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p,
+                                                 C.c_void_p, C.c_void_p, C.c_int32]
+        L.escg_ring_group_advance.argtypes = [C.POINTER(_H), C.c_int32, C.c_int64]
+        L.escg_ipc_open.argtypes = [C.c_int32, C.c_void_p, _pp]
+        L.escg_ipc_close.argtypes = [C.c_int32, C.c_void_p]
     L.escg_simulate.argtypes = [_P, _f64p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64,
                                 C.c_uint32, C.c_int32, C.c_void_p, C.POINTER(C.c_int64), C.c_void_p, C.c_void_p,
                                 C.c_int64, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
     for name in EXPORTS:
-        if name != "escg_dev_last_error" and name != "escg_align_num_randoms":
+        if name != "escg_dev_last_error" and name != "escg_align_num_randoms" and hasattr(L, name):
             getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -245,3 +245,201 @@ class DistributedBand:
                 exchange_halos(*self.halo_views(), self.rank, self.world, self.group)
                 check(lib().escg_dev_band_step(self._h, int(chunk)))
                 done += chunk
+
+
+# ---- multi-part ring: the ring kernel across GPUs -------------------------------------------
+
+def ring_neighbours(part: int, n_parts: int):
+    """(part above, part below) of a periodic ring of parts."""
+    return (part - 1) % n_parts, (part + 1) % n_parts
+
+
+def _part_export(h, ipc: bool):
+    """(planes0, planes1, inbox, rows, ipc handle bytes or None, inbox byte offset) of a ring part."""
+    p0, p1, ib = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    rows, off = C.c_int32(0), C.c_int64(0)
+    buf = (C.c_ubyte * 192)() if ipc else None
+    check(lib().escg_dev_ring_part_export(h, C.byref(p0), C.byref(p1), C.byref(ib), C.byref(rows),
+                                          C.cast(buf, C.c_void_p) if ipc else None, C.byref(off)))
+    return p0.value, p1.value, ib.value, rows.value, (bytes(buf) if ipc else None), off.value
+
+
+class RingGroup:
+    """One lattice as a multi-part ring driven from one process (escg_ring_group_advance).
+
+    Parts on one device run as ONE cooperative launch over all parts — the single-GPU form of the
+    multi-GPU ring: the same kernel, with every cross-part row going through the inbox and plane
+    pointers a part on another GPU would use.  Parts on several devices run one launch each with
+    peer access.  Draws use global coordinates, so any split equals the single-lattice run bit for
+    bit (tests/test_gpu_ring.py)."""
+
+    def __init__(self, params: SimParams, model: DominanceModel, n_parts: int, devices: Optional[Sequence[int]] = None,
+                 ctas: int = 0):
+        if params.seed is None:
+            raise ConfigError("a ring group needs an explicit seed (every part must share it)")
+        self.params, self.model, self.n = params, model, int(n_parts)
+        devices = list(devices) if devices is not None else [0] * self.n
+        if len(devices) != self.n:
+            raise ConfigError("one device per part")
+        if ctas == 0 and len(set(devices)) == 1:
+            # one launch over every part: the parts share the device's SMs
+            try:
+                import torch
+
+                sms = torch.cuda.get_device_properties(devices[0]).multi_processor_count
+            except Exception:
+                sms = 148
+            ctas = max(1, sms // self.n)
+        self._h = []
+        try:
+            for g in range(self.n):
+                h = C.c_void_p()
+                check(lib().escg_dev_create_ring_part(C.byref(params.to_c()),
+                                                      np.ascontiguousarray(model.entries, np.float64),
+                                                      int(model.size), int(model.kind), int(devices[g]), self.n, g,
+                                                      int(ctas), C.byref(h)))
+                self._h.append(h)
+            ex = [_part_export(h, False) for h in self._h]
+            for g, h in enumerate(self._h):
+                up, dn = ring_neighbours(g, self.n)
+                check(lib().escg_dev_ring_part_connect(h, ex[up][0], ex[up][1], ex[up][2], ex[up][3], ex[dn][0],
+                                                       ex[dn][1], ex[dn][2], ex[dn][3]))
+        except Exception:
+            self.close()
+            raise
+        self.info = [BandGroup._band_info(h) for h in self._h]
+
+    close = BandGroup.close
+    __enter__ = BandGroup.__enter__
+    __exit__ = BandGroup.__exit__
+    __del__ = BandGroup.__del__
+    init_lattice = BandGroup.init_lattice
+    set_lattice = BandGroup.set_lattice
+    get_lattice = BandGroup.get_lattice
+    counts = BandGroup.counts
+
+    def describe(self, part: int = 0):
+        v = [C.c_int32(0) for _ in range(4)]
+        check(lib().escg_dev_describe(self._h[part], *[C.byref(x) for x in v]))
+        fmt = C.c_int32(0)
+        check(lib().escg_dev_draw_format(self._h[part], C.byref(fmt)))
+        return dict(kernel={1: "tile", 2: "block", 3: "ring"}[v[0].value], ctas=v[1].value, threads=v[2].value,
+                    smem_bytes=v[3].value, draw_code=fmt.value)
+
+    def advance(self, n_mcs: int):
+        arr = (C.c_void_p * self.n)(*[h.value for h in self._h])
+        check(lib().escg_ring_group_advance(arr, self.n, int(n_mcs)))
+
+    def last_ms(self) -> float:
+        ms, n = C.c_double(0), C.c_int64(0)
+        check(lib().escg_dev_last_timing(self._h[0], C.byref(ms), C.byref(n)))
+        return ms.value
+
+
+def exchange_part_info(mine, rank: int, world: int, group=None):
+    """All-gather every rank's ring-part export (IPC handles, inbox offset, rows) and return the
+    entries of this rank's part above and below."""
+    import torch.distributed as dist
+
+    allv = [None] * world
+    dist.all_gather_object(allv, mine, group=group)
+    up, dn = ring_neighbours(rank, world)
+    return allv[up], allv[dn]
+
+
+class DistributedRing:
+    """This rank's part of one lattice as a multi-part ring, one process per GPU.
+
+    The parts' ring kernels exchange boundary rows with each other inside the kernel, every colour
+    phase, through tagged system-scope stores into the neighbour part's inbox (CUDA IPC mappings of
+    the neighbours' allocations over NVLink): advance() enqueues one launch and returns; nothing on
+    the host takes part in the exchange.  Reads and writes of the lattice synchronise every rank."""
+
+    def __init__(self, params: SimParams, model: DominanceModel, rank: int, world: int, device: int = 0, ctas: int = 0,
+                 group=None):
+        import torch
+        import torch.distributed as dist
+
+        if params.seed is None:
+            raise ConfigError("a ring needs an explicit seed (every part must share it)")
+        if world < 2:
+            raise ConfigError("a distributed ring needs at least 2 ranks")
+        self.params, self.model, self.rank, self.world, self.device, self.group = params, model, rank, world, device, group
+        self._opened = []
+        h = C.c_void_p()
+        check(lib().escg_dev_create_ring_part(C.byref(params.to_c()), np.ascontiguousarray(model.entries, np.float64),
+                                              int(model.size), int(model.kind), int(device), int(world), int(rank),
+                                              int(ctas), C.byref(h)))
+        self._h = h
+        try:
+            _, _, _, rows, ipc, off = _part_export(h, True)
+            up, dn = exchange_part_info((ipc, off, rows), rank, world, group)
+            cache = {}
+
+            def open_part(entry):
+                key = entry[0]
+                if key not in cache:
+                    ptrs = []
+                    for k in range(3):
+                        p = C.c_void_p()
+                        check(lib().escg_ipc_open(int(device), entry[0][64 * k:64 * (k + 1)], C.byref(p)))
+                        self._opened.append(p.value)
+                        ptrs.append(p.value)
+                    cache[key] = (ptrs[0], ptrs[1], ptrs[2] + entry[1], entry[2])
+                return cache[key]
+
+            u, d = open_part(up), open_part(dn)
+            check(lib().escg_dev_ring_part_connect(h, u[0], u[1], u[2], u[3], d[0], d[1], d[2], d[3]))
+        except Exception:
+            self.close()
+            raise
+        self.info = BandGroup._band_info(h)
+        self._torch, self._dist = torch, dist
+
+    def close(self):
+        for p in self._opened:
+            lib().escg_ipc_close(int(self.device), p)
+        self._opened = []
+        if getattr(self, "_h", None):
+            lib().escg_dev_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def _quiesce(self):
+        """Every rank's launches done: the neighbours' last rows are in this part's planes."""
+        self._torch.cuda.synchronize(self.device)
+        self._dist.barrier(group=self.group)
+
+    def init_lattice(self):
+        self._quiesce()
+        check(lib().escg_dev_init_lattice(self._h))
+        self._dist.barrier(group=self.group)
+
+    def set_band(self, band_cells, mcs: int = 0):
+        """This part's rows (rows x L int32) at MCS `mcs` (every rank, before the next advance)."""
+        self._quiesce()
+        part = np.ascontiguousarray(np.asarray(band_cells).ravel(), np.int32)
+        check(lib().escg_dev_set_lattice(self._h, 0, part, int(mcs)))
+        self._dist.barrier(group=self.group)
+
+    def get_band(self) -> np.ndarray:
+        self._quiesce()
+        part = np.zeros(self.info["rows"] * self.params.length, np.int32)
+        m = C.c_int64(0)
+        check(lib().escg_dev_get_lattice(self._h, 0, part.ctypes.data_as(C.c_void_p), C.byref(m)))
+        return part
+
+    def counts(self) -> np.ndarray:
+        self._quiesce()
+        c = np.zeros(self.model.size + 1, np.uint64)
+        check(lib().escg_dev_counts(self._h, 0, c))
+        return c
+
+    def advance(self, n_mcs: int):
+        """Enqueue n_mcs MCS as one ring launch on this rank's GPU; returns without waiting."""
+        check(lib().escg_dev_advance(self._h, int(n_mcs)))

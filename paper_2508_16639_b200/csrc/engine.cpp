@@ -216,6 +216,12 @@ struct escg_dev {
     // SLICED single lattices on the persistent ring kernel (ring.cu): bands, shared memory, mailboxes
     bool ring = false;
     int ring_nb = 0, ring_smem = 0, ring_mbs = 0;
+    // one part of a multi-part ring (escg_dev_create_ring_part): a row band whose ring kernel
+    // exchanges boundary rows with the neighbouring parts' kernels through their inboxes
+    bool ring_part = false, ring_connected = false;
+    bool ring_chain = false;  // the state is a ring launch's: the neighbours flag their rows into it
+    uint32_t ring_epoch = 0;  // ring launches since creation (identical on every part of a ring)
+    escgd::RingPart rpart{};
     int bh_max = 0, bw_max = 0;
     int seam_np = 0;  // block kernel on a periodic lattice with seams: colour phases per MCS (4, 6, 9)
     int phase_table = 0;  // block kernel: per-launch phase-geometry table (few items per thread)
@@ -491,13 +497,23 @@ void band_sync_bytes(escg_dev* h) {
     if (!h->planes_live) return;
     const int c = h->cur[0];
     CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, c, h->lat[c].p, h->H, h->L, h->npl, 1, h->stream));
-    h->planes_live = false;
+    // a ring part's planes stay the state (its neighbours read and write them across devices)
+    if (!h->ring_part) h->planes_live = false;
 }
 void band_sync_planes(escg_dev* h) {
     if (h->planes_live) return;
     const int c = h->cur[0];
     CK(escgd::launch_to_planes(h->lat[c].p, h->pl[c].p, h->H, h->L, h->npl, 1, h->stream));
     h->planes_live = true;
+}
+
+// A ring part's state set from the host: planes now (a neighbour's next launch reads this part's
+// rows from them), and no boundary-row flags to wait for at the next launch.
+void ring_part_fresh(escg_dev* h) {
+    if (!h->ring_part) return;
+    band_sync_planes(h);
+    CK(cudaStreamSynchronize(h->stream));
+    h->ring_chain = false;
 }
 
 void check_replica(escg_dev* h, int r) {
@@ -572,6 +588,116 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
 
 // Ring path: the whole advance (record = 0; final lattice in plane buffer 1) or run (records at
 // t0 + k*interval and at the limit; record k in plane buffer k & 1, named by cur) in one launch.
+// Ring launches of parts p[0..n): `together` = all on one device in ONE cooperative launch (the
+// single-GPU form of the multi-GPU ring: the same kernel, cross-part traffic through the same
+// inbox and plane pointers); otherwise one launch per part on its own device and stream, nothing
+// synchronised between them (the kernels meet through their tagged inbox words).
+void ring_parts_advance(escg_dev** p, int n, int64_t n_mcs, bool together) {
+    if (n_mcs < 0) config_error("mcs count must be non-negative");
+    for (int g = 0; g < n; ++g) {
+        escg_dev* h = p[g];
+        if (!h || !h->ring_part) config_error("not a ring part");
+        if (!h->ring_connected) config_error("ring part not connected to its neighbours (escg_dev_ring_part_connect)");
+        if (h->mcs[0] != p[0]->mcs[0] || h->cur[0] != p[0]->cur[0] || h->ring_epoch != p[0]->ring_epoch ||
+            h->ring_chain != p[0]->ring_chain)
+            config_error("ring parts are out of step");
+    }
+    if (n_mcs == 0) return;
+    if (n_mcs > (int64_t{1} << 29)) config_error("ring launch too long (tags count 4 phases per MCS in 31 bits)");
+    escgd::RingArgs a{};
+    auto fill = [&](escg_dev* h) {
+        a.seeds = h->d_seeds.p;
+        a.rule = rule_args(h);
+        a.run = run_args(h, 0, 1, 0, 0, false);
+        a.H = h->Hg;  // the draws use global rows
+        a.L = h->L;
+        a.S = h->S;
+        a.npl = h->npl;
+        a.K = h->K;
+        a.mcs0 = h->mcs[0];
+        a.mcs_end = h->mcs[0] + n_mcs;
+        a.record = 0;
+        a.mbs = h->ring_mbs;
+        a.acc = h->d_acc.p;
+        a.ticket = h->d_ticket.p;
+        a.T3 = nullptr;
+        a.cur = h->cur[0];
+        a.xset = static_cast<int>(h->ring_epoch & 1u);
+        a.epoch = h->ring_epoch;
+        a.wait_snap = h->ring_chain ? 1 : 0;
+    };
+    // per part: planes current, local mailboxes cleared, and the inbox set of the NEXT launch
+    // cleared (the neighbours write it from their next launch on; this launch's set was cleared
+    // by the previous one, before any neighbour could have started this launch)
+    for (int g = 0; g < n; ++g) {
+        escg_dev* h = p[g];
+        CK(cudaSetDevice(h->device));
+        band_sync_planes(h);
+        const size_t local = static_cast<size_t>(h->ring_nb) * 4 * h->ring_mbs;
+        const int nx = static_cast<int>((h->ring_epoch + 1) & 1u);
+        CK(cudaMemsetAsync(h->d_mbox.p, 0, sizeof(unsigned long long) * local, h->stream));
+        CK(cudaMemsetAsync(h->rpart.inbox + static_cast<size_t>(nx) * 4 * h->ring_mbs, 0,
+                           sizeof(unsigned long long) * 4 * h->ring_mbs, h->stream));
+        CK(cudaMemsetAsync(h->rpart.inbox + static_cast<size_t>(8) * h->ring_mbs + nx * 2, 0,
+                           sizeof(unsigned long long) * 2, h->stream));
+        CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
+    }
+    if (together) {
+        int smem = 0, ctas = 0;
+        for (int g = 0; g < n; ++g) {
+            if (p[g]->device != p[0]->device) config_error("a single-launch ring group needs one device");
+            smem = std::max(smem, p[g]->ring_smem);
+            CK(cudaSetDevice(p[g]->device));
+            CK(cudaStreamSynchronize(p[g]->stream));
+        }
+        fill(p[0]);
+        a.nparts = n;
+        a.smem_bytes = smem;
+        for (int g = 0; g < n; ++g) {
+            a.part[g] = p[g]->rpart;
+            a.part[g].cta0 = ctas;
+            ctas += p[g]->ring_nb;
+        }
+        CK(cudaSetDevice(p[0]->device));
+        if (ctas > escgd::ring_capacity(p[0]->npl, smem, p[0]->device))
+            config_error("ring group does not fit one device (" + std::to_string(ctas) + " co-resident CTAs): fewer CTAs per part");
+        timed_begin(p[0]);
+        CK(escgd::launch_ring(a, ctas, p[0]->stream));
+        timed_end(p[0], 1);
+    } else {
+        for (int g = 0; g < n; ++g) {
+            escg_dev* h = p[g];
+            CK(cudaSetDevice(h->device));
+            fill(h);
+            a.nparts = 1;
+            a.smem_bytes = h->ring_smem;
+            a.part[0] = h->rpart;
+            a.part[0].cta0 = 0;
+            if (n == 1) timed_begin(h);
+            CK(escgd::launch_ring(a, h->ring_nb, h->stream));
+        }
+        if (n == 1) {
+            // one rank's part: device-ordered, the host does not wait (timings read lazily)
+            CK(cudaEventRecord(p[0]->ev1, p[0]->stream));
+            p[0]->last_launches = 1;
+        } else {
+            for (int g = 0; g < n; ++g) {
+                CK(cudaSetDevice(p[g]->device));
+                CK(cudaStreamSynchronize(p[g]->stream));
+            }
+        }
+    }
+    CK(cudaGetLastError());
+    for (int g = 0; g < n; ++g) {
+        escg_dev* h = p[g];
+        h->cur[0] ^= 1;
+        h->mcs[0] += n_mcs;
+        ++h->ring_epoch;
+        h->ring_chain = true;
+        h->planes_live = true;
+    }
+}
+
 void enqueue_ring(escg_dev* h, int64_t t0, int64_t t1, int record, const escgd::RunArgs& run) {
     escgd::RingArgs a{};
     a.pin = h->pl[0].p;
@@ -864,6 +990,7 @@ int64_t escg_align_num_randoms(int64_t requested, int64_t cells) {
 namespace {
 struct BandSpec {
     int nbands = 1, band = 0, kmcs = 2;
+    int ring = 0, ctas = 0;  // multi-part ring: this part's bands (0: one per SM, >= 8 rows each)
 };
 
 void create_impl(const escg_params* p, const double* dominance, int32_t species, int32_t kind, int32_t device,
@@ -886,6 +1013,19 @@ int escg_dev_create_band(const escg_params* p, const double* dominance, int32_t 
         bs.band = band;
         bs.kmcs = kmcs > 0 ? kmcs : 2;
         create_impl(p, dominance, species, kind, device, 1, nullptr, ESCG_KERNEL_BLOCK, out, &bs);
+    });
+}
+
+int escg_dev_create_ring_part(const escg_params* p, const double* dominance, int32_t species, int32_t kind,
+                              int32_t device, int32_t n_parts, int32_t part, int32_t n_ctas, escg_dev** out) {
+    return guarded([&] {
+        BandSpec bs;
+        bs.nbands = n_parts;
+        bs.band = part;
+        bs.kmcs = 1;
+        bs.ring = 1;
+        bs.ctas = n_ctas;
+        create_impl(p, dominance, species, kind, device, 1, nullptr, ESCG_KERNEL_RING, out, &bs);
     });
 }
 
@@ -938,6 +1078,8 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             if (bs->nbands < 2) config_error("a band engine needs at least 2 bands");
             if (bs->band < 0 || bs->band >= bs->nbands) config_error("band index out of range");
             if (bs->kmcs < 1 || bs->kmcs > escgd::kMaxBlockMcs) config_error("band chunk (kmcs) must be in [1, 4]");
+            if (bs->ring && bs->nbands > escgd::kMaxRingParts)
+                config_error("a multi-part ring has at most " + std::to_string(escgd::kMaxRingParts) + " parts");
             if (!(h->flux && h->H % 4 == 0 && h->L % 4 == 0)) config_error("band sharding needs a periodic lattice with L, H divisible by 4");
             if (n_replicas != 1) config_error("band engines hold one lattice");
             const int u = h->H / 4;
@@ -945,7 +1087,10 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             h->band = bs->band;
             h->band_start = static_cast<int>(static_cast<int64_t>(u) * bs->band / bs->nbands) * 4;
             h->band_rows = static_cast<int>(static_cast<int64_t>(u) * (bs->band + 1) / bs->nbands) * 4 - h->band_start;
-            h->halo = escgd::margin_rows(bs->kmcs);
+            // a ring part keeps 2 halo rows per side (a slab reaches 1 row above and 2 below its band)
+            h->halo = bs->ring ? 2 : escgd::margin_rows(bs->kmcs);
+            if (bs->ring && h->band_rows < 8)
+                config_error("ring part too thin (" + std::to_string(h->band_rows) + " rows < 8): use fewer parts");
             if (h->band_rows < h->halo)
                 config_error("band too thin for the halo (" + std::to_string(h->band_rows) + " rows < " +
                              std::to_string(h->halo) + "): use fewer bands or a smaller chunk");
@@ -1069,7 +1214,8 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
             if (const char* kv = std::getenv("ESCG_BLOCK_MCS")) kmax = std::max(1, std::min(kmax, std::atoi(kv)));
             if (bs) kmax = bs->kmcs;  // chunks may not outgrow the band's halo
             if (h->narrow == 2) {
-                plan_slices(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax, bs != nullptr);
+                if (!(bs && bs->ring))
+                    plan_slices(h.get(), prop.multiProcessorCount, std::min(smem_cap, 200 * 1024), kmax, bs != nullptr);
                 const size_t words = static_cast<size_t>(h->H) * h->npl * (h->L / 128) * 4 * n_replicas;
                 h->pl[0].alloc(words);
                 h->pl[1].alloc(words);
@@ -1119,6 +1265,35 @@ void create_impl(const escg_params* p, const double* dominance, int32_t species,
                 } else if (kernel == ESCG_KERNEL_RING) {
                     config_error("lattice not eligible for the ring kernel (L/128 <= 32, H >= 16, co-resident bands)");
                 }
+            }
+            if (bs && bs->ring) {
+                // one part of a multi-part ring: bands of >= 8 rows of this part, co-resident (the
+                // group emulation on one device checks the sum of its parts at launch)
+                const int GL = h->L / 128;
+                int nb = bs->ctas > 0 ? bs->ctas : prop.multiProcessorCount;
+                nb = std::min(nb, h->band_rows / 8);
+                int coop = 0;
+                CK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+                const int rsmem = nb >= 1 ? escgd::ring_smem_bytes(h->band_rows, h->L, h->npl, nb) : 0;
+                if (!(h->narrow == 2 && coop && nb >= 1 && GL <= 32 && rsmem <= std::min(smem_cap, 200 * 1024) &&
+                      nb <= escgd::ring_capacity(h->npl, rsmem, device)))
+                    config_error("lattice not eligible for a multi-part ring (bit-sliced, L/128 <= 32, parts of >= 8 rows)");
+                h->ring = true;
+                h->ring_part = true;
+                h->sliced3 = false;
+                h->ring_nb = nb;
+                h->ring_smem = rsmem;
+                h->ring_mbs = 2 + 3 * h->npl * GL * 4;
+                const size_t local = static_cast<size_t>(nb) * 4 * h->ring_mbs;
+                h->d_mbox.alloc(local + escgd::kRingInboxWords(h->ring_mbs));
+                CK(cudaMemset(h->d_mbox.p, 0, sizeof(unsigned long long) * h->d_mbox.n));
+                h->rpart.pl[0] = h->pl[0].p;
+                h->rpart.pl[1] = h->pl[1].p;
+                h->rpart.mbox = h->d_mbox.p;
+                h->rpart.inbox = h->d_mbox.p + local;
+                h->rpart.r0 = h->band_start;
+                h->rpart.rows = h->band_rows;
+                h->rpart.nb = nb;
             }
             h->d_acc.alloc(static_cast<size_t>(h->S1) * n_replicas);
             h->d_ticket.alloc(n_replicas);
@@ -1180,6 +1355,7 @@ int escg_dev_init_lattice(escg_dev* h) {
         std::fill(h->mcs.begin(), h->mcs.end(), 0);
         std::fill(h->cur.begin(), h->cur.end(), 0);
         h->planes_live = false;
+        ring_part_fresh(h);
     });
 }
 
@@ -1200,6 +1376,7 @@ int escg_dev_set_lattice(escg_dev* h, int32_t replica, const int32_t* cells, int
         if (bad) throw Error(ESCG_EENGINE, "corrupt lattice value (outside [0, S])");
         h->mcs[replica] = mcs;
         h->planes_live = false;
+        ring_part_fresh(h);
     });
 }
 
@@ -1237,6 +1414,10 @@ int escg_dev_counts(escg_dev* h, int32_t replica, uint64_t* out) {
 int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
     return guarded([&] {
         if (!h) config_error("null handle");
+        if (h->ring_part) {  // this process's part of a multi-part ring (one rank per GPU)
+            ring_parts_advance(&h, 1, n_mcs, false);
+            return;
+        }
         if (h->nbands > 1) config_error("band engines advance through escg_group_advance");
         if (n_mcs < 0) config_error("mcs count must be non-negative");
         CK(cudaSetDevice(h->device));
@@ -1593,6 +1774,92 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
             bands[g]->cur[0] = par;
             bands[g]->last_launches = launch_no;
         }
+    });
+}
+
+int escg_dev_ring_part_export(escg_dev* h, void** planes0, void** planes1, void** inbox, int32_t* rows, void* ipc,
+                              int64_t* inbox_offset) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (!h->ring_part) config_error("not a ring part");
+        CK(cudaSetDevice(h->device));
+        if (planes0) *planes0 = h->rpart.pl[0];
+        if (planes1) *planes1 = h->rpart.pl[1];
+        if (inbox) *inbox = h->rpart.inbox;
+        if (rows) *rows = h->rpart.rows;
+        if (inbox_offset) *inbox_offset = static_cast<int64_t>(reinterpret_cast<char*>(h->rpart.inbox) -
+                                                               reinterpret_cast<char*>(h->d_mbox.p));
+        if (ipc) {  // CUDA IPC handles of the three allocations (planes 0, planes 1, mailboxes)
+            static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+            cudaIpcMemHandle_t m[3];
+            CK(cudaIpcGetMemHandle(&m[0], h->pl[0].p));
+            CK(cudaIpcGetMemHandle(&m[1], h->pl[1].p));
+            CK(cudaIpcGetMemHandle(&m[2], h->d_mbox.p));
+            std::memcpy(ipc, m, sizeof(m));
+        }
+    });
+}
+
+int escg_dev_ring_part_connect(escg_dev* h, void* up_planes0, void* up_planes1, void* up_inbox, int32_t up_rows,
+                               void* dn_planes0, void* dn_planes1, void* dn_inbox, int32_t dn_rows) {
+    return guarded([&] {
+        if (!h) config_error("null handle");
+        if (!h->ring_part) config_error("not a ring part");
+        if (!up_planes0 || !up_planes1 || !up_inbox || !dn_planes0 || !dn_planes1 || !dn_inbox)
+            config_error("null neighbour pointer");
+        if (up_rows < 8 || dn_rows < 8) config_error("neighbour part too thin");
+        h->rpart.up_pl[0] = static_cast<uint32_t*>(up_planes0);
+        h->rpart.up_pl[1] = static_cast<uint32_t*>(up_planes1);
+        h->rpart.up_inbox = static_cast<unsigned long long*>(up_inbox);
+        h->rpart.up_rows = up_rows;
+        h->rpart.dn_pl[0] = static_cast<uint32_t*>(dn_planes0);
+        h->rpart.dn_pl[1] = static_cast<uint32_t*>(dn_planes1);
+        h->rpart.dn_inbox = static_cast<unsigned long long*>(dn_inbox);
+        h->ring_connected = true;
+    });
+}
+
+int escg_ipc_open(int32_t device, const void* handle, void** ptr) {
+    return guarded([&] {
+        if (!handle || !ptr) config_error("null argument");
+        CK(cudaSetDevice(device));
+        cudaIpcMemHandle_t m;
+        std::memcpy(&m, handle, sizeof(m));
+        CK(cudaIpcOpenMemHandle(ptr, m, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+int escg_ipc_close(int32_t device, void* ptr) {
+    return guarded([&] {
+        if (!ptr) config_error("null argument");
+        CK(cudaSetDevice(device));
+        CK(cudaIpcCloseMemHandle(ptr));
+    });
+}
+
+int escg_ring_group_advance(escg_dev** parts, int32_t n, int64_t n_mcs) {
+    return guarded([&] {
+        if (!parts || n < 2) config_error("a ring group needs at least 2 parts");
+        for (int g = 0; g < n; ++g)
+            if (!parts[g] || !parts[g]->ring_part || parts[g]->nbands != n || parts[g]->band != g)
+                config_error("group must list parts 0..n-1 of one ring");
+        bool one = true;
+        for (int g = 0; g < n; ++g) one = one && parts[g]->device == parts[0]->device;
+        if (!one) {  // parts on several GPUs of this process: peer access between ring neighbours
+            for (int g = 0; g < n; ++g)
+                for (int nb : {(g + n - 1) % n, (g + 1) % n}) {
+                    const int d0 = parts[g]->device, d1 = parts[nb]->device;
+                    int can = 0;
+                    if (d0 == d1) continue;
+                    CK(cudaDeviceCanAccessPeer(&can, d0, d1));
+                    if (!can) config_error("ring parts on GPUs without peer access");
+                    CK(cudaSetDevice(d0));
+                    const cudaError_t pe = cudaDeviceEnablePeerAccess(d1, 0);
+                    if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) CK(pe);
+                    cudaGetLastError();
+                }
+        }
+        ring_parts_advance(parts, n, n_mcs, one);
     });
 }
 

@@ -170,6 +170,22 @@ cudaError_t launch_from_planes(const uint32_t* pl0, const uint32_t* pl1, const i
 // full-width rows; colour phases exchange boundary rows with the two neighbour bands through L2
 // mailboxes (data words tagged with the phase), so no area is recomputed.
 constexpr int kRingThreads = 256;
+// One row range of a multi-part ring (csrc/ring.cu "parts"): its bands run on one device, the
+// boundary bands exchange with the neighbouring parts through tagged words in the consumer part's
+// inboxes (NVLink peer stores when the parts sit on different GPUs) and write the rows they finish
+// in a neighbour's range into its plane buffers as well.
+constexpr int kMaxRingParts = 8;
+struct RingPart {
+    uint32_t* pl[2];                // plane buffers, rows [r0 - 2, r0 + rows + 2) (local row = gy - r0 + 2)
+    uint32_t* up_pl[2];             // the part above's (peer memory)
+    uint32_t* dn_pl[2];             // the part below's
+    unsigned long long* mbox;       // local band mailboxes [nb][dir][parity][mbs]
+    unsigned long long* inbox;      // [set][side: 0 from above, 1 from below][parity][mbs], flags [set][side]
+    unsigned long long* up_inbox;   // the part above's inboxes (this part's band 0 publishes there)
+    unsigned long long* dn_inbox;   // the part below's (this part's last band publishes there)
+    int r0, rows, up_rows, nb, cta0;
+};
+
 struct RingArgs {
     const uint32_t* pin;      // input planes [H][NPL][L/128][4]
     uint32_t* pbuf[2];        // snapshots: record k of the launch -> pbuf[k & 1]; advance -> pbuf[1]
@@ -187,7 +203,15 @@ struct RingArgs {
     int smem_bytes;
     int qcap;                 // > 0: per-warp deferred-tile queue capacity override (tests)
     const uint32_t* T3;       // SLICED3 tables (orc_slice3_table layout), null: SLICED
+    // multi-part ring (nparts > 0; advance only): parts [0, nparts) of this launch, CTAs by cta0
+    int nparts;
+    int cur;                  // plane buffer holding the state (the final phase writes cur ^ 1)
+    int xset;                 // inbox set of this launch (launch epoch & 1)
+    uint32_t epoch;           // launch epoch (identical on every part)
+    int wait_snap;            // 1: the previous launch's boundary rows arrive from the neighbours
+    RingPart part[kMaxRingParts];
 };
+constexpr int kRingInboxWords(int mbs) { return 8 * mbs + 4; }  // 2 sets x 2 sides x 2 parities + flags
 cudaError_t launch_ring(const RingArgs& a, int nb, cudaStream_t s);
 int ring_smem_bytes(int H, int L, int npl, int nb);
 int ring_capacity(int npl, int smem_bytes, int device);  // co-resident CTAs (cooperative launch)

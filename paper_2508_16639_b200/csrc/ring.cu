@@ -73,6 +73,25 @@ __device__ __forceinline__ ulonglong2 ld_tag2(const unsigned long long* p) {
     asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
     return v;
 }
+// the same between parts of a multi-part ring (the words cross NVLink: system scope)
+__device__ __forceinline__ void st_tag2_sys(unsigned long long* p, uint32_t a, uint32_t b, uint32_t tag) {
+    const unsigned long long x = (static_cast<unsigned long long>(tag) << 32) | a;
+    const unsigned long long y = (static_cast<unsigned long long>(tag) << 32) | b;
+    asm volatile("st.relaxed.sys.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(x), "l"(y) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_tag2_sys(const unsigned long long* p) {
+    ulonglong2 v;
+    asm volatile("ld.relaxed.sys.global.v2.u64 {%0, %1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t tag_of(unsigned long long x) { return static_cast<uint32_t>(x >> 32); }
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
@@ -90,7 +109,20 @@ struct RingCtx {
     int mbs;
     const uint32_t* T3;   // SLICED3 thresholds T, S in shared memory, null: SLICED
     const uint32_t* T3g;  // the whole SLICED3 table (global)
+    // multi-part ring: this band's part (shared memory), its rows, the launch's inbox set
+    const RingPart* P;    // null: single-device ring (the lattice wraps inside this launch)
+    int pr0, prows, xset, cur;
 };
+
+// Inbox (set, side: 0 rows from the part above, 1 from below, parity) of a part, and its flags
+// (the neighbour's final boundary rows of the previous launch are in this part's planes).
+__device__ __forceinline__ unsigned long long* inbox_slot(unsigned long long* base, int set, int side, int par,
+                                                          int mbs) {
+    return base + static_cast<size_t>((set * 2 + side) * 2 + par) * static_cast<size_t>(mbs);
+}
+__device__ __forceinline__ unsigned long long* inbox_flag(unsigned long long* base, int set, int side, int mbs) {
+    return base + static_cast<size_t>(8) * static_cast<size_t>(mbs) + set * 2 + side;
+}
 
 // Mailbox of band `cta`, direction dir (0: rows shared with the band above, 1: below), parity par.
 __device__ __forceinline__ unsigned long long* mailbox(const RingCtx& C, int cta, int dir, int par) {
@@ -103,11 +135,15 @@ __device__ __forceinline__ int mslot(const RingCtx& C, int s, int p, int g) {
 }
 
 // Publish shared rows s_lo..s_hi (window rows wrow0 + s) into this band's mailbox, then the header.
-template <int NPL>
+template <int NPL, bool PARTS>
 __device__ __forceinline__ void ring_publish(const RingCtx& C, int dir, int wrow0, int s_lo, int s_hi, int par,
                                              uint32_t tag) {
     const int lane = threadIdx.x & 31;
-    unsigned long long* mb = mailbox(C, C.c, dir, par);
+    // the band above / below in another part: into that part's inbox (peer memory)
+    const bool cross = PARTS && (dir == 0 ? C.c == 0 : C.c == C.nb - 1);
+    unsigned long long* mb =
+        !cross ? mailbox(C, C.c, dir, par)
+               : (dir == 0 ? inbox_slot(C.P->up_inbox, C.xset, 1, par, C.mbs) : inbox_slot(C.P->dn_inbox, C.xset, 0, par, C.mbs));
     if (lane < C.GL) {
         for (int s = s_lo; s <= s_hi; ++s) {
 #pragma unroll
@@ -115,24 +151,36 @@ __device__ __forceinline__ void ring_publish(const RingCtx& C, int dir, int wrow
                 const uint4 v = lds128(C.sw + (wrow0 + s) * C.RP + (p * C.GL + lane) * 4);
                 unsigned long long* d = mb + mslot<NPL>(C, s, p, lane);
                 ESCG_CHECK(s >= 0 && s < 3 && mslot<NPL>(C, s, p, lane) + 3 < C.mbs && wrow0 + s <= C.R1 - C.R0 + 2);
-                st_tag2(d, v.x, v.y, tag);
-                st_tag2(d + 2, v.z, v.w, tag);
+                if (cross) {
+                    st_tag2_sys(d, v.x, v.y, tag);
+                    st_tag2_sys(d + 2, v.z, v.w, tag);
+                } else {
+                    st_tag2(d, v.x, v.y, tag);
+                    st_tag2(d + 2, v.z, v.w, tag);
+                }
             }
         }
     }
-    if (lane == 0) st_tag2(mb, 0u, 0u, tag);  // header: this band finished the phase
+    if (lane == 0) {  // header: this band finished the phase
+        if (cross)
+            st_tag2_sys(mb, 0u, 0u, tag);
+        else
+            st_tag2(mb, 0u, 0u, tag);
+    }
 }
 
 // Import the neighbour's shared rows s_lo..s_hi of the previous phase (tag) into window rows
 // wrow0 + s; with nothing to import, wait for its header.  Polls until every word carries the tag.
-template <int NPL>
+template <int NPL, bool PARTS>
 __device__ __forceinline__ void ring_import(const RingCtx& C, int src, int dir, int wrow0, int s_lo, int s_hi, int par,
                                          uint32_t tag, int diag_q) {
     const int lane = threadIdx.x & 31;
-    const unsigned long long* mb = mailbox(C, src, dir, par);
+    const bool cross = PARTS && (dir == 1 ? C.c == 0 : C.c == C.nb - 1);
+    const unsigned long long* mb =
+        cross ? inbox_slot(C.P->inbox, C.xset, dir == 1 ? 0 : 1, par, C.mbs) : mailbox(C, src, dir, par);
     if (s_lo > s_hi) {
         if (lane == 0)
-            while (tag_of(ld_tag2(mb).x) != tag) {
+            while (tag_of((cross ? ld_tag2_sys(mb) : ld_tag2(mb)).x) != tag) {
             }
         __syncwarp();
         return;
@@ -153,8 +201,13 @@ __device__ __forceinline__ void ring_import(const RingCtx& C, int src, int dir, 
             for (int e = 0; e < 3 * NPL; ++e)
                 if ((pend >> e) & 1u) {
                     const unsigned long long* a = mb + mslot<NPL>(C, e / NPL, e % NPL, lane);
-                    v[e][0] = ld_tag2(a);
-                    v[e][1] = ld_tag2(a + 2);
+                    if (cross) {
+                        v[e][0] = ld_tag2_sys(a);
+                        v[e][1] = ld_tag2_sys(a + 2);
+                    } else {
+                        v[e][0] = ld_tag2(a);
+                        v[e][1] = ld_tag2(a + 2);
+                    }
                 }
 #pragma unroll
             for (int e = 0; e < 3 * NPL; ++e)
@@ -327,7 +380,7 @@ struct Exchange {  // one boundary warp's import before / publish after its slab
 // One slab: the tile row anchored at global row w (every group, anchor column residue XR), by one
 // warp.  tbl: this slab's draws precomputed in shared memory ([word][lane]), or null.
 // dst: write the slab's rows there afterwards (and count them into cnt when `count`).
-template <int NPL, int K>
+template <int NPL, int K, bool PARTS>
 __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int xr, uint32_t c1, uint32_t c2s,
                                           uint32_t c2r, const Exchange& X, const uint32_t* tbl, uint32_t* scratch,
                                           uint32_t* dst, bool count, uint32_t (&cnt)[1 << NPL]) {
@@ -348,7 +401,7 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
     RDIAG(X.q, 1, clock64());
     // the draws do not depend on the lattice: the neighbour's rows are awaited only now (before the
     // draw words are loaded, so that few registers are live while polling)
-    if (X.imp) ring_import<NPL>(C, X.src, X.idir, X.iwrow0, X.is_lo, X.is_hi, X.ipar, X.itag,
+    if (X.imp) ring_import<NPL, PARTS>(C, X.src, X.idir, X.iwrow0, X.is_lo, X.is_hi, X.ipar, X.itag,
                                    static_cast<int>(X.q) - 800);
     RDIAG(X.q, 2, clock64());
     uint32_t D[kDrawWords];
@@ -454,12 +507,31 @@ __device__ __forceinline__ void ring_slab(const RingCtx& C, int w, int oy, int x
     __syncwarp();
     RDIAG(X.q, 5, clock64());
 
-    if (X.pub) ring_publish<NPL>(C, X.pdir, X.pwrow0, X.ps_lo, X.ps_hi, X.ppar, X.ptag);
+    if (X.pub) ring_publish<NPL, PARTS>(C, X.pdir, X.pwrow0, X.ps_lo, X.ps_hi, X.ppar, X.ptag);
     if (dst != nullptr && valid) {
         // the slab's rows are final for this phase: snapshot (global rows w-1 .. w+2) and count
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
             int gy = w - 1 + rr;
+            if constexpr (PARTS) {
+                // multi-part ring: local row of this part's planes; rows within one of a part
+                // boundary go to the neighbour's planes as well (it reads them at its next launch)
+                ESCG_CHECK(gy - C.pr0 + 2 >= 1 && gy - C.pr0 + 2 < C.prows + 4);
+#pragma unroll
+                for (int p = 0; p < NPL; ++p) {
+                    const uint4 v = make_uint4(Q[rr][p][0], Q[rr][p][1], Q[rr][p][2], Q[rr][p][3]);
+                    const size_t col = static_cast<size_t>(p * C.GL + lane) * 4;
+                    const size_t rw = static_cast<size_t>(NPL) * C.GL * 4;
+                    __stcg(reinterpret_cast<uint4*>(dst + static_cast<size_t>(gy - C.pr0 + 2) * rw + col), v);
+                    if (C.c == 0 && gy <= C.pr0 + 1)
+                        __stcg(reinterpret_cast<uint4*>(C.P->up_pl[C.cur ^ 1] +
+                                                         static_cast<size_t>(gy - C.pr0 + C.P->up_rows + 2) * rw + col), v);
+                    if (C.c == C.nb - 1 && gy >= C.pr0 + C.prows - 1)
+                        __stcg(reinterpret_cast<uint4*>(C.P->dn_pl[C.cur ^ 1] +
+                                                         static_cast<size_t>(gy - C.pr0 - C.prows + 2) * rw + col), v);
+                }
+                continue;
+            }
             gy = gy < 0 ? gy + C.H : (gy >= C.H ? gy - C.H : gy);
             ESCG_CHECK(gy >= 0 && gy < C.H);
 #pragma unroll
@@ -500,7 +572,7 @@ __device__ __forceinline__ PhaseGeo phase_geo(const Round& rp, int p, int R0, in
     return g;
 }
 
-template <int NPL, int K>
+template <int NPL, int K, bool PARTS>
 __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     extern __shared__ __align__(16) uint32_t sw[];
     __shared__ uint32_t sTh[(kMaxSliceSpecies + 1) * (kMaxSliceSpecies + 1)];
@@ -509,22 +581,65 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     __shared__ uint32_t sCnt[1 << NPL];
     __shared__ int sStop;
     __shared__ uint32_t sT3[64];
+    __shared__ RingPart sPart;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    const int c = blockIdx.x, nb = gridDim.x;
     const int H = a.H, GL = a.L >> 7, S1 = a.S + 1;
-    const int R0 = static_cast<int>(static_cast<int64_t>(c) * H / nb);
-    const int R1 = static_cast<int>(static_cast<int64_t>(c + 1) * H / nb);
+    // multi-part ring: this CTA's part (by first CTA index) and its band within the part
+    int pi = 0;
+#pragma unroll
+    for (int i = 1; i < kMaxRingParts; ++i)
+        if (i < a.nparts && a.part[i].cta0 <= static_cast<int>(blockIdx.x)) pi = i;
+    constexpr bool parts = PARTS;  // multi-part ring instantiation (a.nparts > 0)
+    if (parts && tid == 0) {
+#pragma unroll
+        for (int i = 0; i < kMaxRingParts; ++i)
+            if (i == pi) sPart = a.part[i];
+    }
+    __syncthreads();
+    const int c = parts ? static_cast<int>(blockIdx.x) - sPart.cta0 : static_cast<int>(blockIdx.x);
+    const int nb = parts ? sPart.nb : static_cast<int>(gridDim.x);
+    const int pr0 = parts ? sPart.r0 : 0, prows = parts ? sPart.rows : H;
+    const int R0 = pr0 + static_cast<int>(static_cast<int64_t>(c) * prows / nb);
+    const int R1 = pr0 + static_cast<int>(static_cast<int64_t>(c + 1) * prows / nb);
     const int band = R1 - R0, RP = NPL * GL * 4, per_row = NPL * GL;
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
     for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
     if (a.T3 != nullptr && tid < 64) sT3[tid] = a.T3[tid];
     if (*reinterpret_cast<volatile const int32_t*>(a.run.status) != kStatusRunning) return;  // uniform
 
+    if (parts && a.wait_snap && tid == 0) {
+        // the neighbour parts' last launch wrote the rows they finished in this part's range into
+        // these planes; their flags (release, system scope) say those stores are visible
+        if (c == 0)
+            while (ld_acquire_sys_u64(inbox_flag(sPart.inbox, a.xset, 0, a.mbs)) != a.epoch) {
+            }
+        if (c == nb - 1)
+            while (ld_acquire_sys_u64(inbox_flag(sPart.inbox, a.xset, 1, a.mbs)) != a.epoch) {
+            }
+    }
+    __syncthreads();
     for (int idx = tid; idx < (band + 3) * per_row; idx += nt) {  // rows R0-1 .. R1+1 (mod H)
         const int y = idx / per_row, rem = idx - y * per_row;
         int gy = R0 - 1 + y;
-        gy = gy < 0 ? gy + H : (gy >= H ? gy - H : gy);
-        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(a.pin + (static_cast<size_t>(gy) * per_row + rem) * 4));
+        const uint32_t* src;
+        if (parts) {
+            // halo rows: after a ring launch the neighbours' final rows are already in these planes
+            // (flagged above); after a host write they are read from the neighbours' own rows
+            const uint32_t* base = sPart.pl[a.cur];
+            int lr = gy - pr0 + 2;
+            if (!a.wait_snap && gy < pr0) {
+                base = sPart.up_pl[a.cur];
+                lr = gy - pr0 + sPart.up_rows + 2;
+            } else if (!a.wait_snap && gy >= pr0 + prows) {
+                base = sPart.dn_pl[a.cur];
+                lr = gy - pr0 - prows + 2;
+            }
+            src = base + (static_cast<size_t>(lr) * per_row + rem) * 4;
+        } else {
+            gy = gy < 0 ? gy + H : (gy >= H ? gy - H : gy);
+            src = a.pin + (static_cast<size_t>(gy) * per_row + rem) * 4;
+        }
+        const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src));
         sts128(sw + y * RP + rem * 4, v);
     }
     __syncthreads();
@@ -539,6 +654,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     C.R1 = R1;
     C.c = c;
     C.nb = nb;
+    C.P = parts ? &sPart : nullptr;
+    C.pr0 = pr0;
+    C.prows = prows;
+    C.xset = a.xset;
+    C.cur = a.cur;
     C.lL = lane < GL ? (lane == 0 ? GL - 1 : lane - 1) : lane;
     C.lR = lane < GL ? (lane == GL - 1 ? 0 : lane + 1) : lane;
     C.s32 = seed32(a.seeds[0]);
@@ -547,7 +667,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     C.TK = ~0u << (32 - K);
     C.sT = smem_addr(sTh);
     C.S1 = S1;
-    C.mbox = a.mbox;
+    C.mbox = parts ? sPart.mbox : a.mbox;
     C.mbs = a.mbs;
     C.T3 = a.T3 != nullptr ? sT3 : nullptr;
     C.T3g = a.T3;
@@ -587,7 +707,11 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
                 __syncthreads();
                 if (sStop) return;  // the run ended at record k - 1 (its snapshot is the lattice)
             }
-            uint32_t* dst = snap ? (a.record ? a.pbuf[(rec_k + 1) & 1] : a.pbuf[1]) : nullptr;
+            uint32_t* dst = snap ? (parts ? sPart.pl[a.cur ^ 1] : (a.record ? a.pbuf[(rec_k + 1) & 1] : a.pbuf[1]))
+                                 : nullptr;
+            // a multi-part ring does not publish its last phase: nothing would read it, and so no
+            // store into a neighbour's inbox outlives the launch
+            const int pub = !(parts && snap);
             uint32_t cnt[1 << NPL];
 #pragma unroll
             for (int v = 0; v < (1 << NPL); ++v) cnt[v] = 0u;
@@ -609,7 +733,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
                         X.is_hi = 2 - dT_prev;
                         X.ipar = par ^ 1;
                         X.itag = q;
-                        X.pub = 1;
+                        X.pub = pub;
                         X.pdir = 0;
                         X.pwrow0 = 0;
                         X.ps_lo = 3 - dT;
@@ -626,7 +750,7 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
                         X.is_hi = 2;
                         X.ipar = par ^ 1;
                         X.itag = q;
-                        X.pub = 1;
+                        X.pub = pub;
                         X.pdir = 1;
                         X.pwrow0 = band;
                         X.ps_lo = 0;
@@ -638,7 +762,19 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
                     X.q = q;
                     const int w = g.w0 + 4 * s;
                     const bool cp = snap && a.record;
-                    ring_slab<NPL, K>(C, w, g.oy, g.xr, c1, c2s, c2r, X, tbl, sScr[warp], dst, cp, cnt);
+                    ring_slab<NPL, K, PARTS>(C, w, g.oy, g.xr, c1, c2s, c2r, X, tbl, sScr[warp], dst, cp, cnt);
+                    if (parts && snap && ((s == 0 && warp == 0 && c == 0) || (s == ns - 1 && warp == 1 && c == nb - 1))) {
+                        // this band's final rows in the neighbour part's range are stored: flag them
+                        // for the neighbour's next launch (its inbox set of that launch)
+                        __threadfence_system();
+                        __syncwarp();
+                        if (lane == 0) {
+                            __threadfence_system();
+                            st_release_sys_u64(warp == 0 ? inbox_flag(sPart.up_inbox, a.xset ^ 1, 1, a.mbs)
+                                                         : inbox_flag(sPart.dn_inbox, a.xset ^ 1, 0, a.mbs),
+                                               static_cast<unsigned long long>(a.epoch) + 1ull);
+                        }
+                    }
                 }
             } else if (!(p == 3 && last)) {
                 // producer warps: the next phase's boundary slab draws (top: wtop, bottom: wbot)
@@ -693,9 +829,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     }
 }
 
-template <int NPL, int K>
+template <int NPL, int K, bool PARTS>
 cudaError_t ring_launch_t(const RingArgs& a, int nb, cudaStream_t s) {
-    auto k = ring_kernel<NPL, K>;
+    auto k = ring_kernel<NPL, K, PARTS>;
     static std::atomic<int> configured[kMaxDevices];
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -715,15 +851,15 @@ cudaError_t ring_launch_t(const RingArgs& a, int nb, cudaStream_t s) {
                                        dim3(kRingThreads), args, static_cast<size_t>(a.smem_bytes), s);
 }
 
-template <int NPL>
+template <int NPL, bool PARTS>
 cudaError_t ring_launch_npl(const RingArgs& a, int nb, cudaStream_t s) {
     switch (a.K) {
-        case 6: return ring_launch_t<NPL, 6>(a, nb, s);
-        case 8: return ring_launch_t<NPL, 8>(a, nb, s);
-        case 10: return ring_launch_t<NPL, 10>(a, nb, s);
-        case 12: return ring_launch_t<NPL, 12>(a, nb, s);
-        case 14: return ring_launch_t<NPL, 14>(a, nb, s);
-        case 16: return ring_launch_t<NPL, 16>(a, nb, s);
+        case 6: return ring_launch_t<NPL, 6, PARTS>(a, nb, s);
+        case 8: return ring_launch_t<NPL, 8, PARTS>(a, nb, s);
+        case 10: return ring_launch_t<NPL, 10, PARTS>(a, nb, s);
+        case 12: return ring_launch_t<NPL, 12, PARTS>(a, nb, s);
+        case 14: return ring_launch_t<NPL, 14, PARTS>(a, nb, s);
+        case 16: return ring_launch_t<NPL, 16, PARTS>(a, nb, s);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -731,8 +867,14 @@ cudaError_t ring_launch_npl(const RingArgs& a, int nb, cudaStream_t s) {
 }  // namespace
 
 cudaError_t launch_ring(const RingArgs& a, int nb, cudaStream_t s) {
-    if (a.npl == 2) return ring_launch_npl<2>(a, nb, s);
-    if (a.npl == 3) return ring_launch_npl<3>(a, nb, s);
+    // the multi-part ring is its own instantiation: the single-device kernel keeps its code
+    if (a.nparts > 0) {
+        if (a.npl == 2) return ring_launch_npl<2, true>(a, nb, s);
+        if (a.npl == 3) return ring_launch_npl<3, true>(a, nb, s);
+    } else {
+        if (a.npl == 2) return ring_launch_npl<2, false>(a, nb, s);
+        if (a.npl == 3) return ring_launch_npl<3, false>(a, nb, s);
+    }
     return cudaErrorInvalidValue;
 }
 
@@ -760,8 +902,8 @@ int ring_smem_bytes(int H, int L, int npl, int nb) {
 }
 
 int ring_capacity(int npl, int smem_bytes, int device) {
-    const void* f = npl == 3 ? reinterpret_cast<const void*>(ring_kernel<3, 10>)
-                             : reinterpret_cast<const void*>(ring_kernel<2, 10>);
+    const void* f = npl == 3 ? reinterpret_cast<const void*>(ring_kernel<3, 10, false>)
+                             : reinterpret_cast<const void*>(ring_kernel<2, 10, false>);
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes) != cudaSuccess) return 0;
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kRingThreads, static_cast<size_t>(smem_bytes)) !=

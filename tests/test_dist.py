@@ -122,3 +122,46 @@ def test_band_halo_exchange_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert got == {r: True for r in range(world)}
+
+
+def _ring_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2508_16639_b200.bands import band_rows, exchange_part_info
+
+    # what DistributedRing exchanges: (IPC handles, inbox offset, rows) of every rank's part
+    start, rows = band_rows(4096, world)[rank]
+    mine = (bytes([rank]) * 192, 1000 + rank, rows)
+    up, dn = exchange_part_info(mine, rank, world)
+    q.put((rank, up, dn))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_ring_part_wiring_over_gloo(world):
+    """Each rank of a multi-part ring connects to the part above (rank - 1) and below (rank + 1),
+    periodically, with that rank's own handles, inbox offset and row count."""
+    from paper_2508_16639_b200.bands import band_rows
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_ring_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict()
+    for _ in range(world):
+        r, up, dn = q.get(timeout=120)
+        got[r] = (up, dn)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rows = [r for _, r in band_rows(4096, world)]
+    for r in range(world):
+        u, d = (r - 1) % world, (r + 1) % world
+        assert got[r][0] == (bytes([u]) * 192, 1000 + u, rows[u])
+        assert got[r][1] == (bytes([d]) * 192, 1000 + d, rows[d])

@@ -143,3 +143,88 @@ def test_ring_long_run_equals_block_slice_kernel(escg, monkeypatch, draws):
     assert s1 == s2 == int(escg.RunStatus.Completed)
     assert t1.tolist() == t2.tolist() and np.array_equal(c1, c2)
     assert np.array_equal(l1, l2)
+
+
+# ---- multi-part ring (escg_dev_create_ring_part; bands.RingGroup) ------------------------------
+
+RING_PART_CASES = [
+    # L, H, parts, ctas per part (0: the device's SMs shared by the parts), M
+    (1024, 256, 2, 0, 1e-2),
+    (1024, 256, 3, 0, 1e-2),
+    (1024, 256, 4, 3, 3e-2),   # few fat bands per part: interior slabs too
+    (512, 96, 2, 1, 1e-2),     # one band per part: every band is both boundary bands of its part
+    (3200, 320, 2, 0, 1e-3),   # the bench's row width
+]
+
+
+@pytest.mark.parametrize("case", RING_PART_CASES, ids=[f"{c[0]}x{c[1]}_p{c[2]}_c{c[3]}" for c in RING_PART_CASES])
+def test_ring_parts_match_crs_oracle(escg, oracle, case):
+    """A lattice split into parts whose ring kernels exchange boundary rows through each other's
+    inboxes and planes (one launch over all parts: the single-GPU form of the multi-GPU ring).
+    Consecutive advances alternate the inbox sets and hand the final boundary rows over by flag;
+    a host write in between restarts from the neighbours' rows.  Lattices and counts against the
+    oracle (draw format 2 | K << 8, the same as the single ring's)."""
+    from paper_2508_16639_b200.bands import RingGroup
+
+    L, H, n, ctas, M = case
+    model = escg.make_circulant(3, [1])
+    seed = 4000 + L + n
+    p = _params(escg, L, H, 3, M, 0.1, seed, 100)
+    with RingGroup(p, model, n, ctas=ctas) as grp:
+        d = grp.describe()
+        code = d["draw_code"]
+        assert d["kernel"] == "ring" and code & 0xFF == 2, d
+        grp.init_lattice()
+        init = grp.get_lattice()
+        assert np.array_equal(init, oracle.crs_init(L, H, 3, 0.1, seed))
+        cur, t = init, 0
+        for step in (3, 1, 2, 5):
+            grp.advance(step)
+            cur = oracle.crs_run(cur, L, H, model.matrix(), M, seed, t, step, narrow=code)
+            t += step
+            assert np.array_equal(grp.get_lattice(), cur), ("after MCS", t)
+        assert grp.counts().tolist() == oracle.densities(cur, 3).tolist()
+        # host write between advances: the next launch reads the neighbours' rows directly
+        rng = np.random.default_rng(n)
+        cells = rng.integers(0, 4, L * H).astype(np.int32)
+        grp.set_lattice(cells, mcs=t)
+        grp.advance(2)
+        grp.advance(3)
+        want = oracle.crs_run(cells, L, H, model.matrix(), M, seed, t, 5, narrow=code)
+        assert np.array_equal(grp.get_lattice(), want)
+
+
+def test_ring_parts_equal_single_ring(escg):
+    """40 MCS at the bench's row width: a 4-part ring equals the single-device ring."""
+    from paper_2508_16639_b200.bands import RingGroup
+
+    L, H, M, seed = 3200, 512, 1e-4, 91
+    model = escg.make_circulant(3, [1])
+    p = _params(escg, L, H, 3, M, 0.1, seed, 40)
+    with escg.DeviceEngine(p, model, kernel="ring") as eng:
+        eng.init_lattice()
+        eng.advance(40)
+        want = eng.get_lattice()
+    with RingGroup(p, model, 4) as grp:
+        grp.init_lattice()
+        for _ in range(4):
+            grp.advance(10)
+        got = grp.get_lattice()
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2")
+def test_ring_parts_on_two_gpus(escg, oracle):
+    """Parts on two GPUs of one process: one launch per GPU, rows cross over NVLink peer stores."""
+    from paper_2508_16639_b200.bands import RingGroup
+
+    L, H, M, seed = 1024, 256, 1e-2, 5150
+    model = escg.make_circulant(3, [1])
+    with RingGroup(_params(escg, L, H, 3, M, 0.1, seed, 10), model, 2, devices=[0, 1]) as grp:
+        code = grp.describe()["draw_code"]
+        grp.init_lattice()
+        init = grp.get_lattice()
+        grp.advance(3)
+        grp.advance(4)
+        got = grp.get_lattice()
+    assert np.array_equal(got, oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 7, narrow=code))
