@@ -273,6 +273,48 @@ def band_measurement(e, cfg, model, rank, world, local, args):
         return {"value": None, "error": "%s: %s" % (type(ex).__name__, ex)}
 
 
+def ring_measurement(e, cfg, model, rank, world, local, args):
+    """N > 1: the same lattice as a multi-part ring over the N ranks (bands.DistributedRing: each
+    GPU's ring kernel exchanges its boundary rows with the neighbouring GPUs' kernels inside the
+    launch, every colour phase, through system-scope stores into their inboxes over NVLink).  Device
+    time, max over ranks, of `steps` x 20 MCS (one launch per step); reported inside the line."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_16639_b200 import bands
+
+    L = cfg["L"]
+    if L % 128 or L // 128 > 32 or cfg["S"] > 7 or L // world < 8:
+        return None
+    try:
+        p = e.SimParams(length=L, height=L, species=cfg["S"], mobility=cfg["M"], empty_prob=cfg["p0"], seed=20240601,
+                        mcs_limit=10 ** 12)
+        n = 20
+        with bands.DistributedRing(p, model, rank, world, device=local) as r:
+            r.init_lattice()
+            for _ in range(max(1, args.warmup)):
+                r.advance(n)
+            r.counts()  # synchronises every rank (and raises if an exchange timed out)
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record()
+            for _ in range(args.steps):
+                r.advance(n)
+            ev1.record()
+            r.counts()
+            ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda", dtype=torch.float64)
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+            ms = float(ms.item())
+            info = r.info
+        v = L * L * n * args.steps / (ms / 1e3)
+        return {"value": v, "unit": UNIT, "scaling": "strong", "ms_per_step": ms / args.steps, "mcs_per_step": n,
+                "mcs_per_s": v / (L * L), "rows_per_gpu": info["rows"],
+                "workload": "one L=%d lattice as a %d-part ring (bands.DistributedRing: in-kernel boundary "
+                            "exchange between the GPUs' ring kernels over NVLink, one launch per %d MCS)"
+                            % (L, world, n)}
+    except Exception as ex:  # reported, never fatal to the line
+        return {"value": None, "error": "%s: %s" % (type(ex).__name__, ex)}
+
+
 def run_ours(args):
     import torch
 
@@ -379,6 +421,7 @@ def run_ours(args):
     e2e_value = N * MCS_PER_STEP * args.steps * world / e2e_s
     n_records = MCS_PER_STEP // interval + 1
     band = band_measurement(e, cfg, model, rank, world, local, args) if world > 1 else None
+    ring = ring_measurement(e, cfg, model, rank, world, local, args) if world > 1 else None
 
     if rank == 0:
         peak, peak_src = peak_hbm()
@@ -427,6 +470,8 @@ def run_ours(args):
                                        % summ["mcs_per_launch"]}
         if band is not None:
             line["band"] = band
+        if ring is not None:
+            line["ring"] = ring
         if world == 1 and not args.no_cpu_baseline:
             try:
                 line["cpu_baseline"] = cpu_baseline(cfg)

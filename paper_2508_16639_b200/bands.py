@@ -401,6 +401,13 @@ class DistributedRing:
             lib().escg_ipc_close(int(self.device), p)
         self._opened = []
         if getattr(self, "_h", None):
+            try:  # every rank unmapped this part's buffers before they are freed
+                import torch.distributed as dist
+
+                if dist.is_available() and dist.is_initialized():
+                    dist.barrier(group=self.group)
+            except Exception:
+                pass
             lib().escg_dev_destroy(self._h)
             self._h = None
 

@@ -511,6 +511,7 @@ void band_sync_planes(escg_dev* h) {
 // rows from them), and no boundary-row flags to wait for at the next launch.
 void ring_part_fresh(escg_dev* h) {
     if (!h->ring_part) return;
+    CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
     band_sync_planes(h);
     CK(cudaStreamSynchronize(h->stream));
     h->ring_chain = false;
@@ -588,6 +589,17 @@ int64_t enqueue_block_steps(escg_dev* h, int64_t t, int64_t n, bool count_last, 
 
 // Ring path: the whole advance (record = 0; final lattice in plane buffer 1) or run (records at
 // t0 + k*interval and at the limit; record k in plane buffer k & 1, named by cur) in one launch.
+// A ring part whose launch gave up waiting for a neighbour (kStatusRingTimeout): raise.
+void ring_part_check(escg_dev* h) {
+    if (!h->ring_part) return;
+    int32_t st = 0;
+    CK(cudaMemcpyAsync(&st, h->d_status.p, sizeof(int32_t), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (st == escgd::kStatusRingTimeout)
+        engine_error("multi-part ring: a neighbour part stopped answering (exchange timed out); the lattice is "
+                     "invalid until set_lattice / init_lattice on every part");
+}
+
 // Ring launches of parts p[0..n): `together` = all on one device in ONE cooperative launch (the
 // single-GPU form of the multi-GPU ring: the same kernel, cross-part traffic through the same
 // inbox and plane pointers); otherwise one launch per part on its own device and stream, nothing
@@ -625,6 +637,9 @@ void ring_parts_advance(escg_dev** p, int n, int64_t n_mcs, bool together) {
         a.xset = static_cast<int>(h->ring_epoch & 1u);
         a.epoch = h->ring_epoch;
         a.wait_snap = h->ring_chain ? 1 : 0;
+        a.timeout_ns = escgd::kRingPartTimeoutNs;
+        if (const char* tv = std::getenv("ESCG_RING_TIMEOUT_S"))
+            a.timeout_ns = static_cast<unsigned long long>(std::max(0.001, std::atof(tv)) * 1e9);
     };
     // per part: planes current, local mailboxes cleared, and the inbox set of the NEXT launch
     // cleared (the neighbours write it from their next launch on; this launch's set was cleared
@@ -640,7 +655,7 @@ void ring_parts_advance(escg_dev** p, int n, int64_t n_mcs, bool together) {
                            sizeof(unsigned long long) * 4 * h->ring_mbs, h->stream));
         CK(cudaMemsetAsync(h->rpart.inbox + static_cast<size_t>(8) * h->ring_mbs + nx * 2, 0,
                            sizeof(unsigned long long) * 2, h->stream));
-        CK(cudaMemsetAsync(h->d_status.p, 0xFF, sizeof(int32_t), h->stream));
+        // (the status stays as the last launch left it: a timed-out ring keeps failing until reset)
     }
     if (together) {
         int smem = 0, ctas = 0;
@@ -664,6 +679,7 @@ void ring_parts_advance(escg_dev** p, int n, int64_t n_mcs, bool together) {
         timed_begin(p[0]);
         CK(escgd::launch_ring(a, ctas, p[0]->stream));
         timed_end(p[0], 1);
+        ring_part_check(p[0]);
     } else {
         for (int g = 0; g < n; ++g) {
             escg_dev* h = p[g];
@@ -684,6 +700,7 @@ void ring_parts_advance(escg_dev** p, int n, int64_t n_mcs, bool together) {
             for (int g = 0; g < n; ++g) {
                 CK(cudaSetDevice(p[g]->device));
                 CK(cudaStreamSynchronize(p[g]->stream));
+                ring_part_check(p[g]);
             }
         }
     }
@@ -1386,6 +1403,7 @@ int escg_dev_get_lattice(escg_dev* h, int32_t replica, int32_t* out, int64_t* mc
         check_replica(h, replica);
         CK(cudaSetDevice(h->device));
         band_sync_bytes(h);
+        ring_part_check(h);
         if (out) {
             const int64_t n = owned_cells(h);
             if (h->d_i32.n < static_cast<size_t>(n)) h->d_i32.alloc(n);
@@ -1403,6 +1421,7 @@ int escg_dev_counts(escg_dev* h, int32_t replica, uint64_t* out) {
         check_replica(h, replica);
         CK(cudaSetDevice(h->device));
         band_sync_bytes(h);
+        ring_part_check(h);
         DevBuf<unsigned long long> tmp;
         tmp.alloc(h->S1);
         CK(escgd::launch_count(owned_lat(h, replica), owned_cells(h), 1, h->S, tmp.p, h->stream));

@@ -209,9 +209,15 @@ struct RingArgs {
     int xset;                 // inbox set of this launch (launch epoch & 1)
     uint32_t epoch;           // launch epoch (identical on every part)
     int wait_snap;            // 1: the previous launch's boundary rows arrive from the neighbours
+    unsigned long long timeout_ns;  // a wait for a neighbour part gives up after this long
     RingPart part[kMaxRingParts];
 };
 constexpr int kRingInboxWords(int mbs) { return 8 * mbs + 4; }  // 2 sets x 2 sides x 2 parities + flags
+// a multi-part ring whose neighbour stops answering (a rank that died, a launch that never came)
+// gives up after this long, with this status (every waiting part times out in turn): the host
+// raises instead of hanging
+constexpr unsigned long long kRingPartTimeoutNs = 20ull * 1000 * 1000 * 1000;  // default (ESCG_RING_TIMEOUT_S)
+constexpr int kStatusRingTimeout = 0x5254;
 cudaError_t launch_ring(const RingArgs& a, int nb, cudaStream_t s);
 int ring_smem_bytes(int H, int L, int npl, int nb);
 int ring_capacity(int npl, int smem_bytes, int device);  // co-resident CTAs (cooperative launch)

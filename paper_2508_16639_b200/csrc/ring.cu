@@ -93,6 +93,11 @@ __device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsign
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t tag_of(unsigned long long x) { return static_cast<uint32_t>(x >> 32); }
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -112,7 +117,23 @@ struct RingCtx {
     // multi-part ring: this band's part (shared memory), its rows, the launch's inbox set
     const RingPart* P;    // null: single-device ring (the lattice wraps inside this launch)
     int pr0, prows, xset, cur;
+    int32_t* status;          // multi-part ring: kStatusRingTimeout once any wait gave up
+    unsigned long long t0;    // launch start (global timer, ns)
+    unsigned long long budget;  // ns a multi-part wait may take
 };
+
+// Multi-part ring waits are bounded: past the budget (or once another CTA gave up) a wait
+// returns, the launch runs out with junk rows and the status tells the host.  Checked every 64
+// polls (each poll is an L2 or NVLink round trip anyway).
+__device__ __forceinline__ bool ring_expired(const RingCtx& C, unsigned& polls) {
+    if ((++polls & 63u) != 0u) return false;
+    if (*reinterpret_cast<volatile const int32_t*>(C.status) == kStatusRingTimeout) return true;
+    if (global_ns() - C.t0 > C.budget) {
+        atomicExch(C.status, kStatusRingTimeout);
+        return true;
+    }
+    return false;
+}
 
 // Inbox (set, side: 0 rows from the part above, 1 from below, parity) of a part, and its flags
 // (the neighbour's final boundary rows of the previous launch are in this part's planes).
@@ -178,9 +199,12 @@ __device__ __forceinline__ void ring_import(const RingCtx& C, int src, int dir, 
     const bool cross = PARTS && (dir == 1 ? C.c == 0 : C.c == C.nb - 1);
     const unsigned long long* mb =
         cross ? inbox_slot(C.P->inbox, C.xset, dir == 1 ? 0 : 1, par, C.mbs) : mailbox(C, src, dir, par);
+    unsigned polls = 0;
     if (s_lo > s_hi) {
         if (lane == 0)
             while (tag_of((cross ? ld_tag2_sys(mb) : ld_tag2(mb)).x) != tag) {
+                if constexpr (PARTS)
+                    if (cross && ring_expired(C, polls)) break;
             }
         __syncwarp();
         return;
@@ -196,6 +220,8 @@ __device__ __forceinline__ void ring_import(const RingCtx& C, int src, int dir, 
 #ifdef ESCG_DIAG_RING
             ++rounds;
 #endif
+            if constexpr (PARTS)
+                if (cross && ring_expired(C, polls)) break;
             ulonglong2 v[3 * NPL][2];
 #pragma unroll
             for (int e = 0; e < 3 * NPL; ++e)
@@ -607,15 +633,21 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     if (a.T3 != nullptr && tid < 64) sT3[tid] = a.T3[tid];
     if (*reinterpret_cast<volatile const int32_t*>(a.run.status) != kStatusRunning) return;  // uniform
 
+    const unsigned long long t_start = global_ns();
     if (parts && a.wait_snap && tid == 0) {
         // the neighbour parts' last launch wrote the rows they finished in this part's range into
         // these planes; their flags (release, system scope) say those stores are visible
+        RingCtx T{};
+        T.status = a.run.status;
+        T.t0 = t_start;
+        T.budget = a.timeout_ns;
+        unsigned polls = 0;
         if (c == 0)
-            while (ld_acquire_sys_u64(inbox_flag(sPart.inbox, a.xset, 0, a.mbs)) != a.epoch) {
-            }
+            while (ld_acquire_sys_u64(inbox_flag(sPart.inbox, a.xset, 0, a.mbs)) != a.epoch)
+                if (ring_expired(T, polls)) break;
         if (c == nb - 1)
-            while (ld_acquire_sys_u64(inbox_flag(sPart.inbox, a.xset, 1, a.mbs)) != a.epoch) {
-            }
+            while (ld_acquire_sys_u64(inbox_flag(sPart.inbox, a.xset, 1, a.mbs)) != a.epoch)
+                if (ring_expired(T, polls)) break;
     }
     __syncthreads();
     for (int idx = tid; idx < (band + 3) * per_row; idx += nt) {  // rows R0-1 .. R1+1 (mod H)
@@ -659,6 +691,9 @@ __global__ void __launch_bounds__(kRingThreads, 1) ring_kernel(RingArgs a) {
     C.prows = prows;
     C.xset = a.xset;
     C.cur = a.cur;
+    C.status = a.run.status;
+    C.t0 = t_start;
+    C.budget = a.timeout_ns;
     C.lL = lane < GL ? (lane == 0 ? GL - 1 : lane - 1) : lane;
     C.lR = lane < GL ? (lane == GL - 1 ? 0 : lane + 1) : lane;
     C.s32 = seed32(a.seeds[0]);

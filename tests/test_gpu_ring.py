@@ -228,3 +228,23 @@ def test_ring_parts_on_two_gpus(escg, oracle):
         grp.advance(4)
         got = grp.get_lattice()
     assert np.array_equal(got, oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 7, narrow=code))
+
+
+def test_ring_part_without_neighbour_times_out(escg, monkeypatch):
+    """One rank's part launched while its neighbour never runs (a dead rank): the kernel's bounded
+    waits give up (ESCG_RING_TIMEOUT_S) and the host raises instead of hanging."""
+    import ctypes as C
+
+    from paper_2508_16639_b200 import _lib
+    from paper_2508_16639_b200.bands import RingGroup
+
+    monkeypatch.setenv("ESCG_RING_TIMEOUT_S", "0.5")
+    p = _params(escg, 1024, 128, 3, 1e-2, 0.1, 77, 10)
+    with RingGroup(p, escg.make_circulant(3, [1]), 2) as grp:
+        grp.init_lattice()
+        h = grp._h[0]
+        _lib.check(_lib.lib().escg_dev_advance(h, 2))  # part 1 never launches
+        out = np.zeros(64 * 1024, np.int32)
+        m = C.c_int64(0)
+        with pytest.raises(escg.EngineError, match="stopped answering"):
+            _lib.check(_lib.lib().escg_dev_get_lattice(h, 0, out.ctypes.data_as(C.c_void_p), C.byref(m)))
