@@ -395,6 +395,9 @@ class DistributedRing:
             raise
         self.info = BandGroup._band_info(h)
         self._torch, self._dist = torch, dist
+        # the part's launches go on torch's current stream: CUDA events there bracket them
+        self._stream = torch.cuda.current_stream(device)
+        check(lib().escg_dev_set_stream(h, C.c_void_p(self._stream.cuda_stream)))
 
     def close(self):
         for p in self._opened:
