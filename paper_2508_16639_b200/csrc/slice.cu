@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     uint32_t* dst = a.pdst + r * NW;
     __shared__ uint32_t sCnt[1 << NPL];
     __shared__ int sLast;
+    __shared__ __align__(8) unsigned long long sMbar;
     if (tid < (1 << NPL)) sCnt[tid] = 0u;
     if (tid < 3) sQn[tid] = 0u;
     for (int i = tid; i < S1 * S1; i += nt) sTh[i] = a.rule.T[i];
@@ -337,6 +338,31 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (a.run.status[r] != kStatusRunning) return;  // uniform per CTA
 
+#ifndef ESCG_SLICE_NO_TMA
+    // the window by TMA: one bulk copy per (row, plane) run of Gw groups (two when the run wraps
+    // around the row), completion counted in bytes on one mbarrier
+    const uint32_t mbar = smem_addr(&sMbar);
+    if (tid == 0) {
+        tma_mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        tma_expect_tx(mbar, static_cast<uint32_t>(Wh) * NPL * Gw * 16u);
+    }
+    __syncthreads();
+    {
+        const int n1 = gs0 + Gw <= GL ? Gw : GL - gs0;  // groups before the row wraps
+        const uint32_t sw0 = smem_addr(sw);
+        for (int idx = tid; idx < Wh * NPL; idx += nt) {
+            const int y = idx / NPL, p = idx - y * NPL;
+            int gy = wy0 + y;
+            gy = bigy ? gy % Hg : (gy >= Hg ? gy - Hg : gy);
+            const uint32_t* srow = src + static_cast<size_t>(gy * NPL + p) * GL * 4;
+            const uint32_t d = sw0 + static_cast<uint32_t>((y * RP + p * Gw * 4) * 4);
+            tma_g2s(d, srow + gs0 * 4, static_cast<uint32_t>(n1) * 16u, mbar);
+            if (n1 < Gw) tma_g2s(d + n1 * 16u, srow, static_cast<uint32_t>(Gw - n1) * 16u, mbar);
+        }
+    }
+    tma_wait(mbar, 0);
+#else
     for (int idx = tid; idx < Wh * per_row; idx += nt) {
         const int y = idx / per_row, rem = idx - y * per_row;
         const int p = rem / Gw, gw = rem - p * Gw;
@@ -348,6 +374,7 @@ __global__ void __launch_bounds__(slice_threads(LPI), slice_min_blocks(LPI)) sli
         sts128(sw + y * RP + rem * 4, v);
     }
     __syncthreads();
+#endif
 
     if (a.step) {
         SliceCtx C;

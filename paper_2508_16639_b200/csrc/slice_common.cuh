@@ -230,6 +230,28 @@ namespace {
 // conditional-run rows C[m][g] serve only masks with two or more undecided tiles.
 __device__ __forceinline__ uint32_t word_of(const uint4 w, int a) { return a == 0 ? w.x : (a == 1 ? w.y : (a == 2 ? w.z : w.w)); }
 
+// ---- TMA bulk copies of plane rows (cp.async.bulk + mbarrier) ----------------------------------
+__device__ __forceinline__ void tma_mbar_init(uint32_t mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count));
+}
+__device__ __forceinline__ void tma_expect_tx(uint32_t mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_wait(uint32_t mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred done;\n"
+        "TWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+        "@!done bra TWAIT_%=;\n\t}" ::"r"(mbar),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(mbar)
+                 : "memory");
+}
+
 // A mask with at least two undecided tiles, the first at G (probability ~ 5e-4 per attempt at K = 10).
 __device__ __noinline__ uint32_t slice3_multi(int G, int a, uint32_t item, uint32_t c1, uint32_t c2s, uint32_t s32,
                                               const uint32_t* sT, const uint32_t* gT) {
