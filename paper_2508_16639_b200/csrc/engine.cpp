@@ -375,7 +375,10 @@ void plan_slices(escg_dev* h, int sms, int smem_cap, int kmax, bool fixk) {
     const int GL = h->L / 128, uy = h->rows_count / 4;  // band engines: the band's rows only
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
-    double overhead = 20000.0;  // launch + window load/store, in cell units
+    // launch + window load/store + wave tail, in cell units; fitted on B200 with the TMA window
+    // load at L=16384: k = 1 1.52e12, k = 2 1.67e12 attempts/s; 1e5-2e5 picks k = 2, 3.8e5 k = 4
+    // (1.49e12), the old 2e4 k = 1
+    double overhead = 120000.0;
     if (const char* o = std::getenv("ESCG_SLICE_OVERHEAD")) overhead = std::atof(o);
     const int kforce = fixk ? kmax : (std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0);
     for (int k = 1; k <= kmax; ++k) {
