@@ -308,7 +308,11 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax, bool fixk) {
     const int ry_extra = h->rows_count - uy * 4, rx_extra = h->L - ux * cu;
     double best = 1e300;
     int bnby = 1, bnbx = 1, bk = 1;
-    const double kOverheadCells = 40000.0;  // launch + window load/store, measured on B200
+    // launch + window load/store per launch, in cell units (measured on B200): 4e4 for
+    // the L=3200-size blocks; smaller windows load faster, so the weight falls with the window
+    // (15000 + 0.3 cells per window cell, capped at 4e4): one L=1000 lattice then runs 2 MCS per
+    // launch (8.7e10 vs 8.0e10 attempts/s at 4), one L=200 lattice 3 (6.0e9 vs 5.7e9)
+    const double kOverheadCells = 40000.0;
     // band engines keep the chunk they were created for (its halo depth, and every band of a lattice
     // must exchange halos at the same cadence); ESCG_BLOCK_K is an experiment knob for the rest
     const int kforce = fixk ? kmax : (std::getenv("ESCG_BLOCK_K") ? std::atoi(std::getenv("ESCG_BLOCK_K")) : 0);
@@ -323,7 +327,9 @@ void plan_blocks(escg_dev* h, int sms, int smem_cap, int kmax, bool fixk) {
                 const int64_t waves = (ctas + sms - 1) / sms;
                 const double grow = 3.0 * (h->seam_np > 0 ? h->seam_np : 4) * k + 3.0;  // validity margin
                 const double area = (bh + grow) * (bw + grow);
-                const double cost = static_cast<double>(waves) * (area + kOverheadCells / k);
+                const double win = static_cast<double>(bh + 2 * escgd::margin_rows(k)) * (bw + 2 * escgd::margin_cols(k));
+                const double over = std::min(kOverheadCells, 15000.0 + 0.3 * win);
+                const double cost = static_cast<double>(waves) * (area + over / k);
                 if (cost < best * 0.999) {
                     best = cost;
                     bnby = nby;
