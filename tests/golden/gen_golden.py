@@ -284,6 +284,19 @@ def gen_stats2():
     return out
 
 
+def gen_stats3():
+    """C1 at its own length: RPS L=200, M=1e-4, p0=0.1 to 1e4 MCS, 64 reference seeds."""
+    out = {}
+    with Pool(8) as pool:
+        L, M, mcs, nseed, s0 = 200, 1e-4, 10000, 64, 8000
+        res = pool.map(_traj_corr, [(L, M, 0.1, mcs, s0 + s, 500) for s in range(nseed)])
+        out["rps_L200_M1e-4_1e4"] = {"desc": "C1: RPS L=200 M=1e-4 p0=0.1, reference serial engine: counts every "
+                                             "500 MCS to 1e4, final status and correlation length",
+                                     "steps": res[0][1], "counts": [r_[0] for r_ in res],
+                                     "status": [r_[2] for r_ in res], "corr_len": [r_[3] for r_ in res]}
+    return out
+
+
 if __name__ == "__main__":
     def dump(name, obj):
         with open(os.path.join(HERE, name), "w") as f:
@@ -293,6 +306,9 @@ if __name__ == "__main__":
     dump("kat.json", gen_kat())
     dump("serial.json", gen_serial())
     dump("rule.json", gen_rule())
+    if "--stats3" in sys.argv:
+        dump("stats3.json", gen_stats3())
+        sys.exit(0)
     if "--stats2" in sys.argv:
         dump("stats2.json", gen_stats2())
         sys.exit(0)
