@@ -1535,6 +1535,7 @@ int escg_dev_run(escg_dev* h, int64_t mcs_limit, int64_t interval, uint32_t stop
                  int32_t record_trace, int32_t* status_out) {
     return guarded([&] {
         if (!h) config_error("null handle");
+        if (h->ring_part) config_error("ring parts advance through escg_dev_advance / escg_ring_group_advance");
         if (h->nbands > 1) config_error("band engines advance through escg_group_advance");
         CK(cudaSetDevice(h->device));
         const std::vector<int64_t> start(h->mcs);
@@ -1657,6 +1658,7 @@ int escg_group_advance(escg_dev** bands, int32_t n, int64_t n_mcs) {
         for (int g = 0; g < n; ++g) {
             escg_dev* h = bands[g];
             if (!h || h->nbands != n || h->band != g) config_error("group must list bands 0..n-1 of one lattice");
+            if (h->ring_part) config_error("ring parts advance through escg_ring_group_advance");
             if (h->mcs[0] != bands[0]->mcs[0] || h->cur[0] != bands[0]->cur[0] || h->kmcs != bands[0]->kmcs)
                 config_error("bands are out of step");
             if (h->narrow != bands[0]->narrow || h->K != bands[0]->K || h->npl != bands[0]->npl)
@@ -1895,7 +1897,7 @@ int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint
                        int64_t* bytes) {
     return guarded([&] {
         if (!h) config_error("null handle");
-        if (h->nbands < 2) config_error("not a band engine");
+        if (h->nbands < 2 || h->ring_part) config_error("not a band engine");
         CK(cudaSetDevice(h->device));
         uint8_t* base = h->lat[h->cur[0]].p;
         size_t row = static_cast<size_t>(h->L);
@@ -1916,7 +1918,7 @@ int escg_dev_band_rows(escg_dev* h, uint8_t** recv_top, uint8_t** send_top, uint
 int escg_dev_band_step(escg_dev* h, int32_t n_mcs) {
     return guarded([&] {
         if (!h) config_error("null handle");
-        if (h->nbands < 2) config_error("not a band engine");
+        if (h->nbands < 2 || h->ring_part) config_error("not a band engine");
         if (n_mcs < 1 || n_mcs > h->kmcs)
             config_error("band step must run 1.." + std::to_string(h->kmcs) + " MCS (the halo depth)");
         CK(cudaSetDevice(h->device));
