@@ -248,3 +248,23 @@ def test_ring_part_without_neighbour_times_out(escg, monkeypatch):
         m = C.c_int64(0)
         with pytest.raises(escg.EngineError, match="stopped answering"):
             _lib.check(_lib.lib().escg_dev_get_lattice(h, 0, out.ctypes.data_as(C.c_void_p), C.byref(m)))
+
+
+def test_ring_parts_reject_band_entry_points(escg):
+    """A ring part is advanced only by ring launches: run, band step and band-group advance refuse it."""
+    import ctypes as C
+
+    from paper_2508_16639_b200 import _lib
+    from paper_2508_16639_b200.bands import RingGroup
+
+    p = _params(escg, 1024, 128, 3, 1e-2, 0.1, 78, 10)
+    with RingGroup(p, escg.make_circulant(3, [1]), 2) as grp:
+        h = grp._h[0]
+        L = _lib.lib()
+        with pytest.raises(escg.ConfigError, match="ring parts"):
+            _lib.check(L.escg_dev_run(h, 5, 1, 0, -1, 0, None))
+        with pytest.raises(escg.ConfigError, match="not a band engine"):
+            _lib.check(L.escg_dev_band_step(h, 1))
+        arr = (C.c_void_p * 2)(*[x.value for x in grp._h])
+        with pytest.raises(escg.ConfigError, match="ring parts"):
+            _lib.check(L.escg_group_advance(arr, 2, 1))
