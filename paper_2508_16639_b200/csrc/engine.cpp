@@ -2030,7 +2030,8 @@ int escg_simulate(const escg_params* p, const double* dominance, int32_t species
         std::string env;
         for (const char* k : {"ESCG_DRAW_FORMAT", "ESCG_SLICE_K", "ESCG_SLICE_LPI", "ESCG_SLICE_QCAP", "ESCG_SLICE_SPLIT",
                               "ESCG_SLICE_OVERHEAD", "ESCG_BLOCK_MCS", "ESCG_BLOCK_K", "ESCG_BLOCK_THREADS",
-                              "ESCG_PERSISTENT", "ESCG_PHASE_TABLE", "ESCG_TILE_THREADS", "ESCG_WIDE_RULE", "ESCG_RING"}) {
+                              "ESCG_PERSISTENT", "ESCG_PHASE_TABLE", "ESCG_TILE_THREADS", "ESCG_WIDE_RULE", "ESCG_RING",
+                              "ESCG_RING_NB", "ESCG_SLICE_DRAWS"}) {
             const char* v = std::getenv(k);
             env += std::string(k) + "=" + (v ? v : "") + ";";
         }
