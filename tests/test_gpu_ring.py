@@ -148,16 +148,18 @@ def test_ring_long_run_equals_block_slice_kernel(escg, monkeypatch, draws):
 # ---- multi-part ring (escg_dev_create_ring_part; bands.RingGroup) ------------------------------
 
 RING_PART_CASES = [
-    # L, H, parts, ctas per part (0: the device's SMs shared by the parts), M
-    (1024, 256, 2, 0, 1e-2),
-    (1024, 256, 3, 0, 1e-2),
-    (1024, 256, 4, 3, 3e-2),   # few fat bands per part: interior slabs too
-    (512, 96, 2, 1, 1e-2),     # one band per part: every band is both boundary bands of its part
-    (3200, 320, 2, 0, 1e-3),   # the bench's row width
+    # L, H, parts, ctas per part (0: the device's SMs shared by the parts), M, model
+    (1024, 256, 2, 0, 1e-2, "rps"),
+    (1024, 256, 3, 0, 1e-2, "rps"),
+    (1024, 256, 4, 3, 3e-2, "rps"),    # few fat bands per part: interior slabs too
+    (512, 96, 2, 1, 1e-2, "rps"),      # one band per part: every band is both boundary bands of its part
+    (3200, 320, 2, 0, 1e-3, "rps"),    # the bench's row width
+    (1024, 200, 3, 2, 1e-2, "rpsls"),  # 3 bit planes, parts of 64-68 rows, uneven bands
+    (640, 136, 8, 1, 3e-2, "rps"),     # the most parts, 16-20 rows each
 ]
 
 
-@pytest.mark.parametrize("case", RING_PART_CASES, ids=[f"{c[0]}x{c[1]}_p{c[2]}_c{c[3]}" for c in RING_PART_CASES])
+@pytest.mark.parametrize("case", RING_PART_CASES, ids=[f"{c[0]}x{c[1]}_p{c[2]}_c{c[3]}_{c[5]}" for c in RING_PART_CASES])
 def test_ring_parts_match_crs_oracle(escg, oracle, case):
     """A lattice split into parts whose ring kernels exchange boundary rows through each other's
     inboxes and planes (one launch over all parts: the single-GPU form of the multi-GPU ring).
@@ -166,27 +168,28 @@ def test_ring_parts_match_crs_oracle(escg, oracle, case):
     oracle (draw format 2 | K << 8, the same as the single ring's)."""
     from paper_2508_16639_b200.bands import RingGroup
 
-    L, H, n, ctas, M = case
-    model = escg.make_circulant(3, [1])
+    L, H, n, ctas, M, name = case
+    model = _model(escg, name)
+    S = model.size
     seed = 4000 + L + n
-    p = _params(escg, L, H, 3, M, 0.1, seed, 100)
+    p = _params(escg, L, H, S, M, 0.1, seed, 100)
     with RingGroup(p, model, n, ctas=ctas) as grp:
         d = grp.describe()
         code = d["draw_code"]
         assert d["kernel"] == "ring" and code & 0xFF == 2, d
         grp.init_lattice()
         init = grp.get_lattice()
-        assert np.array_equal(init, oracle.crs_init(L, H, 3, 0.1, seed))
+        assert np.array_equal(init, oracle.crs_init(L, H, S, 0.1, seed))
         cur, t = init, 0
         for step in (3, 1, 2, 5):
             grp.advance(step)
             cur = oracle.crs_run(cur, L, H, model.matrix(), M, seed, t, step, narrow=code)
             t += step
             assert np.array_equal(grp.get_lattice(), cur), ("after MCS", t)
-        assert grp.counts().tolist() == oracle.densities(cur, 3).tolist()
+        assert grp.counts().tolist() == oracle.densities(cur, S).tolist()
         # host write between advances: the next launch reads the neighbours' rows directly
         rng = np.random.default_rng(n)
-        cells = rng.integers(0, 4, L * H).astype(np.int32)
+        cells = rng.integers(0, S + 1, L * H).astype(np.int32)
         grp.set_lattice(cells, mcs=t)
         grp.advance(2)
         grp.advance(3)
