@@ -348,6 +348,29 @@ def test_band_group_equals_single_lattice(escg, oracle, n_bands, kmcs, LH):
 
 
 @pytest.mark.gpu
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2")
+@pytest.mark.parametrize("fmt", ["wide", "sliced"])
+def test_band_group_on_two_gpus(escg, oracle, fmt, monkeypatch):
+    """Bands on two GPUs of one process: halos by peer copies between the devices (escg_group_advance),
+    bit-identical to the oracle schedule (byte and bit-sliced kernels)."""
+    from paper_2508_16639_b200.bands import BandGroup
+
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", fmt)
+    L, H, M, seed = 512, 256, 1e-2, 909
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, H, 3, M, 0.1, 4, True, seed=seed)
+    with BandGroup(p, model, 2, devices=[0, 1], kmcs=2) as grp:
+        grp.init_lattice()
+        init = grp.get_lattice()
+        grp.advance(3)
+        grp.advance(4)
+        got = grp.get_lattice()
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        narrow = eng.draw_code()
+    assert np.array_equal(got, oracle.crs_run(init, L, H, model.matrix(), M, seed, 0, 7, narrow=narrow))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("n_bands,kmcs,L,H,S", [(2, 1, 256, 128, 3), (3, 2, 384, 240, 3), (4, 2, 128, 208, 5)])
 def test_sliced_band_group_equals_single_lattice(escg, oracle, n_bands, kmcs, L, H, S, monkeypatch):
     """Row bands on the bit-sliced kernel: the group stays in plane form across chunks (halos move as
