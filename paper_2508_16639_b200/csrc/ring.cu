@@ -30,6 +30,12 @@
 //            runs record_and_check (engine.cpp:47-57).  A CTA reaching record k first waits for
 //            the decision of record k-1 and stops there if the run ended (the lattice of a stop is
 //            that record's snapshot).
+//   parts    (ring_kernel<..., PARTS = true>, advance only) the lattice split into parts, one launch
+//            per part (one GPU each) or one launch over all parts: a part's first and last bands
+//            exchange with the neighbouring part's through tagged system-scope stores into that
+//            part's inbox (two sets, alternate launches), write their final rows into its planes as
+//            well and flag them for its next launch; every cross-part wait is bounded
+//            (kStatusRingTimeout).  DESIGN.md §7.
 #include <cuda_runtime.h>
 
 #include <atomic>
