@@ -219,18 +219,19 @@ def peak_hbm():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def ncu_summary():
-    """Per-launch figures of the dominant kernel from the committed ncu summary (profiles/)."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def ncu_summary(config="C3"):
+    """Per-launch figures of the dominant kernel from the committed ncu summary (profiles/): the ring
+    kernel for C3 (ncu_summary.json), the bit-sliced overlapped-tile kernel for C5."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json" if config == "C3" else "ncu_summary_%s.json" % config)
     try:
         return json.load(open(path))
     except Exception:
         return {}
 
 
-def ncu_traffic():
+def ncu_traffic(config="C3"):
     """DRAM bytes per launch of the dominant kernel (ncu dram__bytes_read + write)."""
-    d = ncu_summary()
+    d = ncu_summary(config)
     return d.get("dram_bytes_per_launch"), d.get("mcs_per_launch")
 
 
@@ -426,7 +427,7 @@ def run_ours(args):
     if rank == 0:
         peak, peak_src = peak_hbm()
         per_gpu = value / world
-        traffic, tr_mcs = ncu_traffic()
+        traffic, tr_mcs = ncu_traffic(args.config)
         kname = {"ring": "ring_kernel (persistent bit-sliced row bands, one launch per step)",
                  "block": ("slice_kernel (bit-sliced overlapped-tile CRS, %d MCS/launch)" % desc.get("kmcs", 1)
                            if desc.get("draw_format") == "sliced"
@@ -435,14 +436,14 @@ def run_ours(args):
                  "tile": "tile_kernel (SMEM-resident lattice, persistent)"}[desc["kernel"]]
         roof = {"bound": "hbm", "achieved": per_gpu * 2 / 1e9, "peak": peak, "unit": "GB/s",
                 "frac": per_gpu * 2 / 1e9 / peak, "peak_source": peak_src,
-                "traffic": traffic if args.config == "C3" else None,
+                "traffic": traffic,
                 "kernel": kname,
                 "algorithmic_bytes": "2 B per site-update attempt (1 B read + 1 B write of the uint8 lattice per "
                                      "site per MCS); achieved = attempts/s x 2 B over the device-timed region"
                                      + ("; during a run the lattice is held as 2-bit planes (0.5 B per attempt moved)"
                                         if desc.get("draw_format") == "sliced" else ""),
                 "avg_launch_us": total_ms / max(launches, 1) * 1e3,
-                "traffic_per_launch_mcs": tr_mcs if args.config == "C3" else None}
+                "traffic_per_launch_mcs": tr_mcs}
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": value / published_rate(cfg) if published_rate(cfg) else None,
@@ -458,7 +459,7 @@ def run_ours(args):
                 "gpu_launches": launches, "roofline": roof, "clocks": clk.summary()}
         # the binding limit: warp-instruction issue (148 SMs x 4 schedulers x 1 instr/clk); warp
         # instructions per attempt from the committed ncu capture of this kernel and launch shape
-        summ = ncu_summary() if args.config == "C3" else {}
+        summ = ncu_summary(args.config)
         clocks = line["clocks"]
         if summ.get("warp_inst_per_launch") and summ.get("mcs_per_launch") and clocks.get("sm_mhz"):
             wipa = summ["warp_inst_per_launch"] / (summ["mcs_per_launch"] * N)
@@ -466,8 +467,9 @@ def run_ours(args):
             line["issue"] = {"bound": "warp-instruction issue", "warp_inst_per_attempt": wipa,
                              "achieved": per_gpu * wipa, "peak": peak_issue, "unit": "warp instr/s",
                              "frac": per_gpu * wipa / peak_issue,
-                             "source": "ncu smsp__inst_executed.sum of one %d-MCS launch (profiles/ncu_summary.json)"
-                                       % summ["mcs_per_launch"]}
+                             "source": "ncu smsp__inst_executed.sum of one %d-MCS launch (profiles/%s)"
+                                       % (summ["mcs_per_launch"], "ncu_summary.json" if args.config == "C3"
+                                          else "ncu_summary_%s.json" % args.config)}
         if band is not None:
             line["band"] = band
         if ring is not None:
