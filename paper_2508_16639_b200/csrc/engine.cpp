@@ -479,8 +479,14 @@ void upload_mcs(escg_dev* h) {
 }
 
 // Block path: bring every replica's lattice into buffer 0 so one launch serves all replicas.
+// A single bit-sliced lattice (overlapped-tile kernel) keeps its state in bit planes between
+// run/advance calls (pl[cur]); byte readers convert on demand (band_sync_bytes).
+bool planes_resident(const escg_dev* h) {
+    return h->narrow == 2 && !h->ring && h->nbands <= 1 && h->nrep == 1 && h->kernel == ESCG_KERNEL_BLOCK;
+}
+
 void normalize_buffers(escg_dev* h) {
-    if (h->kernel != ESCG_KERNEL_BLOCK) return;
+    if (h->kernel != ESCG_KERNEL_BLOCK || h->planes_live) return;  // live planes: the bytes are stale
     for (int r = 0; r < h->nrep; ++r) {
         if (h->cur[r] != 0) {
             CK(cudaMemcpyAsync(h->lat[0].p + static_cast<size_t>(r) * h->N, h->lat[1].p + static_cast<size_t>(r) * h->N,
@@ -841,7 +847,10 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         CK(cudaMemsetAsync(h->d_acc.p, 0, sizeof(unsigned long long) * h->S1 * h->nrep, h->stream));
         CK(cudaMemsetAsync(h->d_ticket.p, 0, sizeof(unsigned int) * h->nrep, h->stream));
         const int64_t t0 = h->mcs[0];
-        int64_t launch_no = 0;
+        // a resident plane state (planes_resident) starts from its own buffer, with no conversion
+        const bool live = h->planes_live && h->narrow == 2 && !h->ring;
+        const int pc = live ? h->cur[0] : 0;
+        int64_t launch_no = h->narrow == 2 ? pc : 0;
         // record at the starting MCS (record_and_check before any step, engine.cpp:181)
         escgd::BlockArgs a{};
         a.src = h->lat[0].p;
@@ -875,15 +884,19 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         a.smem_bytes = h->smem;
         if (h->narrow == 2) {
             // SLICED: the run works on bit planes; the record at the start counts them
-            CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
-            a.psrc = h->pl[0].p;
-            a.pdst = h->pl[1].p;
+            if (!live) {
+                CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+                ++launches;
+            }
+            a.psrc = h->pl[pc].p;
+            a.pdst = h->pl[1 - pc].p;
+            a.dst_index = 1 - pc;  // count-only: the record names buffer pc
             a.K = h->K;
             a.npl = h->npl;
             a.lpi = h->lpi;
             a.qcap = h->qcap;
             CK(escgd::launch_slice(a, h->nrep, h->stream));
-            launches += 2;
+            ++launches;
         } else {
             CK(escgd::launch_block(a, h->nrep, h->threads, h->stream));
             ++launches;
@@ -930,7 +943,7 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
                 poll_pending = true;
             }
         }
-        if (h->narrow == 2) {
+        if (h->narrow == 2 && !planes_resident(h)) {
             // back to bytes: the plane buffer named by the last record (cur = 2 + index)
             CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, h->d_cur.p, 0, h->lat[0].p, h->H, h->L, h->npl,
                                          h->nrep, h->stream));
@@ -938,6 +951,12 @@ void run_impl(escg_dev* h, int64_t limit, int64_t interval, uint32_t flags, int 
         }
     }
     timed_end(h, launches);
+    if (planes_resident(h)) {  // the state stays in the plane buffer the last record names
+        int32_t c = 0;
+        CK(cudaMemcpy(&c, h->d_cur.p, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        h->cur[0] = c >= 2 ? c - 2 : h->cur[0];
+        h->planes_live = true;
+    }
     CK(cudaGetLastError());
     std::vector<int32_t> st(h->nrep);
     CK(cudaMemcpy(h->mcs.data(), h->d_mcs.p, sizeof(int64_t) * h->nrep, cudaMemcpyDeviceToHost));
@@ -1512,19 +1531,28 @@ int escg_dev_advance(escg_dev* h, int64_t n_mcs) {
                                              h->nrep, h->stream));
                 launches = 3;
             } else if (h->narrow == 2 && n_mcs > 0) {
-                CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
-                launches = 1 + enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
-                CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, static_cast<int>(launch_no & 1),
-                                             h->lat[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
-                ++launches;
-                launch_no = 0;  // the lattice is back in byte buffer 0
+                const bool live = h->planes_live;
+                launch_no = live ? h->cur[0] : 0;
+                if (!live) {
+                    CK(escgd::launch_to_planes(h->lat[0].p, h->pl[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+                    ++launches;
+                }
+                launches += enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
+                if (planes_resident(h)) {
+                    h->planes_live = true;  // the state stays in plane buffer launch_no & 1
+                } else {
+                    CK(escgd::launch_from_planes(h->pl[0].p, h->pl[1].p, nullptr, static_cast<int>(launch_no & 1),
+                                                 h->lat[0].p, h->H, h->L, h->npl, h->nrep, h->stream));
+                    ++launches;
+                    launch_no = 0;  // the lattice is back in byte buffer 0
+                }
             } else if (h->narrow != 2) {
                 launches = enqueue_block_steps(h, t0, n_mcs, false, run, launch_no);
             }
             timed_end(h, launches);
             for (int r = 0; r < h->nrep; ++r) {
                 h->mcs[r] += n_mcs;
-                h->cur[r] = static_cast<int>(launch_no & 1);
+                if (n_mcs > 0 || h->narrow != 2) h->cur[r] = static_cast<int>(launch_no & 1);
             }
         }
         CK(cudaGetLastError());
@@ -1541,7 +1569,9 @@ int escg_dev_run(escg_dev* h, int64_t mcs_limit, int64_t interval, uint32_t stop
         const std::vector<int64_t> start(h->mcs);
         run_impl(h, mcs_limit, interval, stop_flags, tracked_species, record_trace != 0, status_out);
         (void)start;
-        if (h->kernel == ESCG_KERNEL_BLOCK && h->narrow == 2)
+        if (planes_resident(h))
+            ;  // the state stays in plane buffer cur[0] (run_impl)
+        else if (h->kernel == ESCG_KERNEL_BLOCK && h->narrow == 2)
             std::fill(h->cur.begin(), h->cur.end(), 0);  // converted back into byte buffer 0
         else if (h->kernel == ESCG_KERNEL_BLOCK)
             CK(cudaMemcpy(h->cur.data(), h->d_cur.p, sizeof(int32_t) * h->nrep, cudaMemcpyDeviceToHost));
@@ -1586,6 +1616,8 @@ int escg_dev_replay(escg_dev* h, const uint32_t* w_cell, const uint32_t* w_dir, 
         if (!h || !w_cell || !w_dir || !w_act) config_error("null argument");
         if (n < 0) config_error("attempt count must be non-negative");
         CK(cudaSetDevice(h->device));
+        band_sync_bytes(h);
+        normalize_buffers(h);
         DevBuf<uint32_t> wc, wd, wa;
         wc.alloc(std::max<int64_t>(n, 1));
         wd.alloc(std::max<int64_t>(n, 1));

@@ -854,3 +854,37 @@ def test_band_steps_ordered_on_the_caller_stream(escg, fmt, monkeypatch):
     finally:
         for b in bands:
             b.close()
+
+
+@pytest.mark.gpu
+def test_sliced_state_stays_in_planes_across_calls(escg, oracle, monkeypatch):
+    """A single bit-sliced lattice keeps its state in bit planes between run/advance calls (no
+    conversion per call); every mix of run, advance, reads, counts and host writes must still be the
+    oracle's schedule."""
+    monkeypatch.setenv("ESCG_DRAW_FORMAT", "sliced")
+    L, H, M, seed = 512, 128, 1e-2, 4321
+    model = escg.make_circulant(3, [1])
+    p = params(escg, L, H, 3, M, 0.1, 4, True, seed=seed)
+    D = model.matrix()
+    with escg.DeviceEngine(p, model, kernel="block") as eng:
+        code = eng.draw_code()
+        assert code & 0xFF in (2, 3)
+        eng.init_lattice()
+        cur = eng.get_lattice()
+        t = 0
+        for op, n in (("run", 5), ("advance", 3), ("advance", 2), ("run", 4), ("get", 0), ("run", 3), ("advance", 1)):
+            if op == "run":
+                st = eng.run(t + n, interval=2)
+                assert int(st[0]) == int(escg.RunStatus.Completed)
+            elif op == "advance":
+                eng.advance(n)
+            if n:
+                cur = oracle.crs_run(cur, L, H, D, M, seed, t, n, narrow=code)
+                t += n
+            if op == "get" or op == "advance":
+                assert np.array_equal(eng.get_lattice(), cur), (op, t)
+        assert np.array_equal(eng.counts(), np.bincount(cur, minlength=4).astype(np.uint64))
+        cells = np.random.default_rng(3).integers(0, 4, L * H).astype(np.int32)
+        eng.set_lattice(cells, mcs=t)
+        eng.advance(2)
+        assert np.array_equal(eng.get_lattice(), oracle.crs_run(cells, L, H, D, M, seed, t, 2, narrow=code))
